@@ -1,0 +1,109 @@
+/*
+ * qgpu.h — extensions of the C-ABI beyond QuEST's names (libqgpu.so).
+ *
+ * Everything here is plain C: pointers, sizes, integers. The reference has no
+ * equivalent for most of these (they expose B200 execution control); where it
+ * has one, it is cited (paths under /root/reference/proj).
+ */
+#ifndef QGPU_EXT_H
+#define QGPU_EXT_H
+
+#include "QuEST.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ----------------------------------------------------------------- errors */
+/* Error classes mirror the reference's exception types (types.hpp:31-55). */
+enum qgpuErrorCode {
+    QGPU_OK = 0,
+    QGPU_DOMAIN_ERROR = 1,   /* qsim::DomainError: invalid argument, no mutation */
+    QGPU_RESOURCE_ERROR = 2, /* qsim::ResourceError: allocation, bytes named */
+    QGPU_COMM_ERROR = 3,     /* qsim::CommError: transport failure, ranks named */
+    QGPU_DEVICE_ERROR = 4    /* CUDA runtime failure */
+};
+typedef void (*qgpuErrorHandler)(const char* errMsg, const char* errFunc, int code,
+                                 void* user);
+/* Replaces the default recording handler (NULL restores it). */
+void qgpuSetErrorHandler(qgpuErrorHandler handler, void* user);
+/* Code of the last error on this thread (0 = none); copies its message. */
+int qgpuGetLastError(char* buf, int len);
+void qgpuClearError(void);
+
+/* ------------------------------------------------------ execution control */
+const char* qgpuVersion(void);
+/* Kernel launches issued by the library since load. */
+unsigned long long qgpuKernelLaunches(void);
+/* HBM passes / exchange rounds executed for this register. */
+unsigned long long qgpuPassCount(Qureg qureg);
+/* Launch every queued op of this register now (stream-ordered, async). */
+void qgpuFlush(Qureg qureg);
+/* Fusion policy for registers of this env: mode 0 = fused HBM passes
+ * (default), 1 = one fused-pass launch per op, 2 = one simple per-gate kernel
+ * per op (the unfused kernel family). maxOps <= 0 keeps the current value,
+ * regQubits in [1,5] (<= 0 keeps). */
+void qgpuSetFusion(QuESTEnv env, int mode, int maxOps, int regQubits);
+/* The CUDA stream (cudaStream_t) all work of this env is enqueued on. */
+void* qgpuGetStream(QuESTEnv env);
+int qgpuGetDevice(QuESTEnv env);
+
+/* Launch profiling: while on, every hot-kernel launch (fused pass, simple
+ * gate, exchange round, depolarise, reduction) is bracketed by a CUDA event
+ * pair on the env's stream. Stop syncs and returns the record count, filling
+ * up to maxRecords durations (ms) and kinds (0 pass, 1 simple, 2 exchange,
+ * 3 depolarise, 4 reduce). */
+void qgpuProfileStart(QuESTEnv env);
+int qgpuProfileStop(QuESTEnv env, double* ms, int* kinds, int maxRecords);
+
+/* --------------------------------------------------------- bulk state I/O */
+/* Interleaved (re, im) doubles of flat amplitudes [start, start + num). */
+void qgpuCopyStateToHost(Qureg qureg, long long int start, long long int num, double* out);
+void qgpuCopyStateFromHost(Qureg qureg, long long int start, long long int num,
+                           const double* in);
+/* Any 2x2 matrix (not checked for unitarity, as the reference allows
+ * untagged matrices, gates.hpp:9-11) on `target` with controls `ctrlMask`:
+ * apply_controlled_gate (kernels.cpp:105-112) / apply_gate_to_density. */
+void qgpuApplyMatrix(Qureg qureg, int target, unsigned long long ctrlMask, const double* m8);
+/* Reference-named reductions: Register::norm_squared (register.cpp:62-75,
+ * compensated) and trace (density.cpp:147-154). */
+qreal qgpuNormSquared(Qureg qureg);
+Complex qgpuTrace(Qureg qureg);
+
+/* ------------------------------------------------------------ distributed */
+/* 2^k virtual ranks on this one GPU, each holding its own chunk, exchanging
+ * through the same sub-chunked protocol as NCCL ranks (a device-side
+ * InProcessTransport, transport.hpp:33-62). numRanks must be a power of 2. */
+QuESTEnv qgpuCreateLoopbackEnv(int numRanks);
+/* One process per GPU over NCCL (loaded at run time: the libnccl.so.2
+ * already in the process, else the system one). Rank 0 calls
+ * qgpuGetNcclUniqueId and distributes the 128 bytes. */
+int qgpuGetNcclUniqueId(char* out128);
+QuESTEnv qgpuCreateNcclEnv(int rank, int numRanks, int device, const char* uniqueId128);
+/* Exchange sub-chunk size in amplitudes (power of two, default 2^24). */
+void qgpuSetExchangeChunk(QuESTEnv env, long long int amps);
+/* Messages / bytes this process's ranks sent for `qureg` (CommStats,
+ * distributed.hpp:63-74); arrays of length numRanks (loopback) or 1. */
+void qgpuCommStats(Qureg qureg, unsigned long long* messages, unsigned long long* bytes);
+
+/* Pure host planner used by every transport (testable without a GPU).
+ * For a gate on flat qubit `target` with controls `ctrlMask` on a
+ * 2^flatQubits vector split over 2^rankLog2 ranks (distributed.cpp:31-57,
+ * 141-169): returns 0 = local, 1 = skip (a rank-bit control fails),
+ * 2 = exchange with *peer; *ownLo = this rank owns the low half of each pair;
+ * *lowMask = controls below the local qubit count. Returns -1 on invalid
+ * input. */
+int qgpuPlanGate(int flatQubits, int rankLog2, int rank, int target,
+                 unsigned long long ctrlMask, int* peer, int* ownLo,
+                 unsigned long long* lowMask);
+/* Exchange schedule: number of sub-chunks and their size for a local length
+ * and requested chunk (the PerAmplitude strategy with block = chunk,
+ * distributed.cpp:215-231). */
+int qgpuPlanChunks(unsigned long long localLen, unsigned long long chunkAmps,
+                   unsigned long long* chunkLen);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* QGPU_EXT_H */

@@ -1,0 +1,339 @@
+/*
+ * qsim_oracle.c — CPU restatement of the reference's state-vector /
+ * density-matrix gate path. TEST INFRASTRUCTURE ONLY: it is the checker the
+ * CUDA product is compared against; only tests/, __graft_entry__.smoke() and
+ * bench.py's cpu_baseline leg may load it. The product never links it.
+ *
+ * Pinning: tests/test_oracle.py runs this restatement and the UNMODIFIED
+ * reference (compiled in place by oracle/Makefile into oracle/_ref/) on the
+ * same seeded op streams and requires bit-identical amplitudes, and checks it
+ * against the SPEC.md known-answer examples in tests/golden/.
+ *
+ * Functions restated from the reference (file:line under
+ * /root/reference/proj):
+ *   orc_pair_base_index   include/qsim/detail/pair_math.hpp:56-61
+ *   orc_apply_gate        src/kernels.cpp:43-59 + pair_math.hpp:30-54
+ *   orc_apply_dm_gate     src/density.cpp:85-116 (G at t, conj G at t+N)
+ *   orc_dephase           src/density.cpp:48-60, 118-130
+ *   orc_depolarise        src/density.cpp:62-81, 132-145
+ *   orc_trace             src/density.cpp:147-154
+ *   orc_norm_naive        src/register.cpp:62-75 (the reference's naive sum)
+ *   orc_splitmix64_next   src/circuit.cpp:16-34
+ *   orc_combine           src/distributed.cpp:174-187 (exchange combine)
+ *
+ * Restated with NO reference implementation ("parity unpinned" — the
+ * reference has no measurement):
+ *   orc_norm_kahan, orc_prob_of_outcome, orc_collapse, orc_measure,
+ *   orc_seed, orc_uniform. These follow the QuEST semantics named in
+ *   BASELINE.json's north star with compensated (Kahan) summation.
+ */
+#include "oracle_ops.h"
+
+#include <math.h>
+#include <stddef.h>
+#include <stdint.h>
+#include <string.h>
+
+/* ---------------------------------------------------------------- indices */
+
+/* pair_math.hpp:56-61 — floor(i / 2^t) * 2^(t+1) + (i mod 2^t). */
+uint64_t orc_pair_base_index(uint64_t i, int target) {
+    const uint64_t low_mask = (UINT64_C(1) << target) - 1;
+    return ((i & ~low_mask) << 1) | (i & low_mask);
+}
+
+/* density.cpp:25-28 */
+static uint64_t insert_zero_bit(uint64_t x, int pos) {
+    const uint64_t low = x & ((UINT64_C(1) << pos) - 1);
+    return ((x >> pos) << (pos + 1)) | low;
+}
+
+/* ------------------------------------------------------------ pair update */
+
+/* pair_math.hpp:30-36. The reference is built with -O3 and FMA available,
+ * so GCC contracts the expression; the contraction it emits (read from the
+ * reference objects' x86: vfmsub231sd / vfmadd231sd /
+ * vfnmadd231sd) is written out here explicitly so this restatement — and the
+ * CUDA kernels, which use the same fma chain — round exactly like the
+ * reference:
+ *   re = fma(-b_im, hi, fma(b_re, hr, fma(a_re, lr, -(a_im * li))))
+ *   im = fma( b_im, hr, fma(b_re, hi, fma(a_re, li,   a_im * lr)))
+ * i.e. the first product of each sum is fused, the second rounded.      */
+static inline void pair_lo_out(const double* lo, const double* hi,
+                               const double* m, double* out) {
+    const double lr = lo[0], li = lo[1], hr = hi[0], hi_ = hi[1];
+    out[0] = fma(-m[3], hi_, fma(m[2], hr, fma(m[0], lr, -(m[1] * li))));
+    out[1] = fma(m[3], hr, fma(m[2], hi_, fma(m[0], li, m[1] * lr)));
+}
+
+/* pair_math.hpp:39-45 */
+static inline void pair_hi_out(const double* lo, const double* hi,
+                               const double* m, double* out) {
+    const double lr = lo[0], li = lo[1], hr = hi[0], hi_ = hi[1];
+    out[0] = fma(-m[7], hi_, fma(m[6], hr, fma(m[4], lr, -(m[5] * li))));
+    out[1] = fma(m[7], hr, fma(m[6], hi_, fma(m[4], li, m[5] * lr)));
+}
+
+/* kernels.cpp:43-59: every pair whose base index holds all control bits. */
+void orc_apply_gate(double* amps, int nq, int target, uint64_t ctrl_mask,
+                    const double* m) {
+    const uint64_t num_pairs = UINT64_C(1) << (nq - 1);
+    const uint64_t off = UINT64_C(1) << target;
+    for (uint64_t i = 0; i < num_pairs; ++i) {
+        const uint64_t base = orc_pair_base_index(i, target);
+        if ((base & ctrl_mask) != ctrl_mask)
+            continue;
+        double* lo = amps + 2 * base;
+        double* hi = amps + 2 * (base + off);
+        double nl[2], nh[2];
+        pair_lo_out(lo, hi, m, nl);
+        pair_hi_out(lo, hi, m, nh);
+        lo[0] = nl[0]; lo[1] = nl[1];
+        hi[0] = nh[0]; hi[1] = nh[1];
+    }
+}
+
+/* density.cpp:85-116: G at ket qubit t with ket controls, then conj(G) at
+ * bra qubit t+N with the controls shifted by N (gates.cpp:40-44). */
+void orc_apply_dm_gate(double* amps, int n, int target, uint64_t ket_mask,
+                       const double* m) {
+    double conj[8];
+    for (int j = 0; j < 4; ++j) {
+        conj[2 * j] = m[2 * j];
+        conj[2 * j + 1] = -m[2 * j + 1];
+    }
+    orc_apply_gate(amps, 2 * n, target, ket_mask, m);
+    orc_apply_gate(amps, 2 * n, target + n, ket_mask << n, conj);
+}
+
+/* density.cpp:48-60: elements whose row/col bits at target differ scale by
+ * (1 - 2p). */
+void orc_dephase(double* amps, int n, int target, double prob) {
+    const int flat = 2 * n;
+    const uint64_t row = UINT64_C(1) << target;
+    const uint64_t col = UINT64_C(1) << (target + n);
+    const double scale = 1.0 - 2.0 * prob;
+    const uint64_t count = UINT64_C(1) << (flat - 2);
+    for (uint64_t u = 0; u < count; ++u) {
+        const uint64_t n00 = insert_zero_bit(insert_zero_bit(u, target), target + n);
+        double* a = amps + 2 * (n00 | row);
+        double* b = amps + 2 * (n00 | col);
+        a[0] *= scale; a[1] *= scale;
+        b[0] *= scale; b[1] *= scale;
+    }
+}
+
+/* density.cpp:62-81: diagonal mix keep/swap, off-diagonal x (1 - 4p/3). */
+void orc_depolarise(double* amps, int n, int target, double prob) {
+    const int flat = 2 * n;
+    const uint64_t row = UINT64_C(1) << target;
+    const uint64_t col = UINT64_C(1) << (target + n);
+    const double keep = 1.0 - 2.0 * prob / 3.0;
+    const double swap = 2.0 * prob / 3.0;
+    const double off = 1.0 - 4.0 * prob / 3.0;
+    const uint64_t count = UINT64_C(1) << (flat - 2);
+    for (uint64_t u = 0; u < count; ++u) {
+        const uint64_t n00 = insert_zero_bit(insert_zero_bit(u, target), target + n);
+        const uint64_t n11 = n00 | row | col;
+        double* p0 = amps + 2 * n00;
+        double* p1 = amps + 2 * n11;
+        const double d0r = p0[0], d0i = p0[1], d1r = p1[0], d1i = p1[1];
+        p0[0] = fma(swap, d1r, keep * d0r);
+        p0[1] = fma(swap, d1i, keep * d0i);
+        p1[0] = fma(swap, d0r, keep * d1r);
+        p1[1] = fma(swap, d0i, keep * d1i);
+        double* a = amps + 2 * (n00 | row);
+        double* b = amps + 2 * (n00 | col);
+        a[0] *= off; a[1] *= off;
+        b[0] *= off; b[1] *= off;
+    }
+}
+
+/* Applies op records in order (the harness op stream). Returns 0, or 1 when
+ * an op is invalid for the register kind (the product's validation is
+ * checked separately against the reference's error behaviour). */
+int orc_run_ops(int nq, int density, int nops, const orc_op* ops, double* amps) {
+    for (int i = 0; i < nops; ++i) {
+        const orc_op* op = ops + i;
+        switch (op->kind) {
+        case ORC_GATE:
+            if (density)
+                orc_apply_dm_gate(amps, nq, op->target, op->ctrl_mask, op->m);
+            else
+                orc_apply_gate(amps, nq, op->target, op->ctrl_mask, op->m);
+            break;
+        case ORC_DEPHASE:
+            if (!density) return 1;
+            orc_dephase(amps, nq, op->target, op->param);
+            break;
+        case ORC_DEPOLARISE:
+            if (!density) return 1;
+            orc_depolarise(amps, nq, op->target, op->param);
+            break;
+        default:
+            return 1;
+        }
+    }
+    return 0;
+}
+
+/* ------------------------------------------------------------- reductions */
+
+/* register.cpp:62-75 — the reference's own (naive, serial) sum. */
+double orc_norm_naive(const double* amps, uint64_t len) {
+    double sum = 0.0;
+    for (uint64_t i = 0; i < len; ++i)
+        sum += amps[2 * i] * amps[2 * i] + amps[2 * i + 1] * amps[2 * i + 1];
+    return sum;
+}
+
+typedef struct { double s, c; } kahan_t;
+
+static inline void kahan_add(kahan_t* k, double x) {
+    const double y = x - k->c;
+    const double t = k->s + y;
+    k->c = (t - k->s) - y;
+    k->s = t;
+}
+
+/* Compensated sum of |a|^2 (calcTotalProb for state vectors, calcPurity for
+ * density matrices). SURVEY.md §7 hard part 2: the naive reference sum is
+ * off by 5.5e-11 at 28 qubits, so parity is taken against this. */
+double orc_norm_kahan(const double* amps, uint64_t len) {
+    kahan_t k = {0.0, 0.0};
+    for (uint64_t i = 0; i < len; ++i)
+        kahan_add(&k, amps[2 * i] * amps[2 * i] + amps[2 * i + 1] * amps[2 * i + 1]);
+    return k.s;
+}
+
+/* density.cpp:147-154: sum of rho_jj at flat j*(2^N + 1). */
+void orc_trace(const double* amps, int n, double* re, double* im) {
+    const uint64_t dim = UINT64_C(1) << n;
+    kahan_t kr = {0.0, 0.0}, ki = {0.0, 0.0};
+    for (uint64_t j = 0; j < dim; ++j) {
+        kahan_add(&kr, amps[2 * (j * (dim + 1))]);
+        kahan_add(&ki, amps[2 * (j * (dim + 1)) + 1]);
+    }
+    *re = kr.s;
+    *im = ki.s;
+}
+
+/* calcProbOfOutcome (restated). State vector: sum |a_i|^2 over i with
+ * bit_t(i) = outcome. Density matrix: sum Re rho_jj over j with
+ * bit_t(j) = outcome. */
+double orc_prob_of_outcome(const double* amps, int nq, int density, int target,
+                           int outcome) {
+    kahan_t k = {0.0, 0.0};
+    if (!density) {
+        const uint64_t len = UINT64_C(1) << nq;
+        for (uint64_t i = 0; i < len; ++i)
+            if ((int)((i >> target) & 1) == outcome)
+                kahan_add(&k, amps[2 * i] * amps[2 * i] + amps[2 * i + 1] * amps[2 * i + 1]);
+    } else {
+        const uint64_t dim = UINT64_C(1) << nq;
+        for (uint64_t j = 0; j < dim; ++j)
+            if ((int)((j >> target) & 1) == outcome)
+                kahan_add(&k, amps[2 * (j * (dim + 1))]);
+    }
+    return k.s;
+}
+
+/* collapseToOutcome (restated): state vector — amplitudes with
+ * bit_t = outcome scale by 1/sqrt(prob), the rest become 0. Density matrix —
+ * rho_jk with bit_t(j) = bit_t(k) = outcome scale by 1/prob, the rest 0. */
+void orc_collapse(double* amps, int nq, int density, int target, int outcome,
+                  double prob) {
+    if (!density) {
+        const uint64_t len = UINT64_C(1) << nq;
+        const double s = 1.0 / sqrt(prob);
+        for (uint64_t i = 0; i < len; ++i) {
+            if ((int)((i >> target) & 1) == outcome) {
+                amps[2 * i] *= s;
+                amps[2 * i + 1] *= s;
+            } else {
+                amps[2 * i] = 0.0;
+                amps[2 * i + 1] = 0.0;
+            }
+        }
+    } else {
+        const uint64_t len = UINT64_C(1) << (2 * nq);
+        const double s = 1.0 / prob;
+        for (uint64_t i = 0; i < len; ++i) {
+            const int r = (int)((i >> target) & 1);
+            const int c = (int)((i >> (target + nq)) & 1);
+            if (r == outcome && c == outcome) {
+                amps[2 * i] *= s;
+                amps[2 * i + 1] *= s;
+            } else {
+                amps[2 * i] = 0.0;
+                amps[2 * i + 1] = 0.0;
+            }
+        }
+    }
+}
+
+/* ------------------------------------------------------------------- RNG */
+
+/* circuit.cpp:20-25 */
+uint64_t orc_splitmix64_next(uint64_t* state) {
+    uint64_t z = (*state += UINT64_C(0x9E3779B97F4A7C15));
+    z = (z ^ (z >> 30)) * UINT64_C(0xBF58476D1CE4E5B9);
+    z = (z ^ (z >> 27)) * UINT64_C(0x94D049BB133111EB);
+    return z ^ (z >> 31);
+}
+
+/* u = (x >> 11) * 2^-53 in [0, 1) (SURVEY.md §7 hard part 3). */
+double orc_uniform(uint64_t* state) {
+    return (double)(orc_splitmix64_next(state) >> 11) * 0x1.0p-53;
+}
+
+/* seedQuEST(seeds, n): state = fold of the seeds through SplitMix64. */
+uint64_t orc_seed(const uint64_t* seeds, int n) {
+    uint64_t st = 0;
+    for (int i = 0; i < n; ++i) {
+        uint64_t tmp = st ^ seeds[i];
+        st = orc_splitmix64_next(&tmp);
+    }
+    return st;
+}
+
+/* measure (restated, QuEST rule): p0 = P(outcome 0); outcome = 1 if
+ * p0 < eps, 0 if 1 - p0 < eps, else (u > p0). Collapses and returns the
+ * outcome; *prob receives the probability of that outcome. */
+int orc_measure(double* amps, int nq, int density, int target, uint64_t* rng,
+                double* prob) {
+    const double eps = 1e-13;
+    const double p0 = orc_prob_of_outcome(amps, nq, density, target, 0);
+    int outcome;
+    if (p0 < eps)
+        outcome = 1;
+    else if (1.0 - p0 < eps)
+        outcome = 0;
+    else
+        outcome = orc_uniform(rng) > p0 ? 1 : 0;
+    const double p = outcome == 0 ? p0 : orc_prob_of_outcome(amps, nq, density, target, 1);
+    orc_collapse(amps, nq, density, target, outcome, p);
+    if (prob) *prob = p;
+    return outcome;
+}
+
+/* ------------------------------------------------------------ distributed */
+
+/* distributed.cpp:174-187: a rank owning chunk `mine` of a communicated gate
+ * combines its amplitudes with the partner's copy `theirs`; only its own half
+ * of each global pair is written. low_mask = controls below the local qubit
+ * count; rank-bit controls are resolved by the caller (:141-145). */
+void orc_combine(double* mine, const double* theirs, uint64_t len,
+                 uint64_t low_mask, int own_lo, const double* m) {
+    for (uint64_t i = 0; i < len; ++i) {
+        if ((i & low_mask) != low_mask)
+            continue;
+        double out[2];
+        if (own_lo)
+            pair_lo_out(mine + 2 * i, theirs + 2 * i, m, out);
+        else
+            pair_hi_out(theirs + 2 * i, mine + 2 * i, m, out);
+        mine[2 * i] = out[0];
+        mine[2 * i + 1] = out[1];
+    }
+}

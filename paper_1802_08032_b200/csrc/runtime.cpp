@@ -1,0 +1,577 @@
+// runtime.cpp — registers in HBM, the fused-pass scheduler, the distributed
+// exchange engine and the compensated reductions.
+//
+// Reference mapping (paths under /root/reference/proj):
+//   QuregImpl / create_register     Register ctor + init, register.cpp:101-130
+//   enqueue/flush/launch_fused      run_circuit's op-by-op dispatch,
+//                                   circuit.cpp:239-247, fused into HBM passes
+//   run_simple                      apply_gate_span, kernels.cpp:43-59
+//   plan_gate                       partition / needs_communication /
+//                                   pair_rank, distributed.cpp:31-57, 141-169
+//   run_exchange_gate               rank_apply_op exchange + combine,
+//                                   distributed.cpp:167-231 (PerAmplitude
+//                                   strategy with block = sub-chunk)
+//   run_depol                       depolarising_pass, density.cpp:62-81
+//                                   (+ its distribution, absent upstream)
+//   reduce_norm / reduce_diag       norm_squared register.cpp:62-75, trace
+//                                   density.cpp:147-154 (compensated)
+#include "runtime.h"
+
+#include "qgpu_kernels.h"
+#include "transport.h"
+
+#include <algorithm>
+#include <cstring>
+
+namespace qgpu {
+
+void cuda_check(cudaError_t e, const char* what) {
+    if (e != cudaSuccess)
+        throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+Env::~Env() {
+    for (QuregImpl* q : std::vector<QuregImpl*>(quregs.begin(), quregs.end())) delete q;
+    nccl.reset();
+    for (auto& r : prof) {
+        cudaEventDestroy(r.start);
+        cudaEventDestroy(r.stop);
+    }
+    for (auto e : event_pool) cudaEventDestroy(e);
+    if (stream) cudaStreamDestroy(stream);
+    if (comm_stream) cudaStreamDestroy(comm_stream);
+}
+
+cudaEvent_t Env::take_event() {
+    if (!event_pool.empty()) {
+        cudaEvent_t e = event_pool.back();
+        event_pool.pop_back();
+        return e;
+    }
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate");
+    return e;
+}
+
+ProfScope::ProfScope(Env* env, int kind) : env_(env), kind_(kind) {
+    if (!env_->profile) return;
+    start_ = env_->take_event();
+    cuda_check(cudaEventRecord(start_, env_->stream), "cudaEventRecord");
+}
+
+ProfScope::~ProfScope() {
+    if (!start_) return;
+    cudaEvent_t stop = env_->take_event();
+    cudaEventRecord(stop, env_->stream);
+    env_->prof.push_back({start_, stop, kind_});
+}
+
+uint8_t classify(const double* m, uint8_t* diag_flags) {
+    auto z = [&](int k) { return m[k] == 0.0; };
+    *diag_flags = 0;
+    if (z(2) && z(3) && z(4) && z(5)) {
+        if (m[0] == 1.0 && z(1)) *diag_flags |= DF_A_ONE;
+        if (m[6] == 1.0 && z(7)) *diag_flags |= DF_D_ONE;
+        return CLS_DIAG;
+    }
+    if (z(0) && z(1) && m[2] == 1.0 && z(3) && m[4] == 1.0 && z(5) && z(6) && z(7))
+        return CLS_SWAP;
+    if (z(1) && z(3) && z(5) && z(7)) return CLS_REAL;
+    if (z(1) && z(2) && z(4) && z(7)) return CLS_RX;
+    return CLS_GENERIC;
+}
+
+int plan_gate(int flat, int rank_log2, int rank, int target, uint64_t cmask, int* peer,
+              int* own_lo, uint64_t* low_mask) {
+    if (flat < 1 || rank_log2 < 0 || rank_log2 > flat || target < 0 || target >= flat ||
+        rank < 0 || rank >= (1 << rank_log2) || ((cmask >> target) & 1u) ||
+        (flat < 64 && (cmask >> flat)))
+        return -1;
+    const int m = flat - rank_log2;
+    const uint64_t local_len = uint64_t{1} << m;
+    *low_mask = cmask & (local_len - 1);
+    *peer = rank;
+    *own_lo = 1;
+    // distributed.cpp:141-145: rank-bit controls resolved from the rank id.
+    const uint64_t rank_mask = m >= 64 ? 0 : (cmask >> m);
+    if ((static_cast<uint64_t>(rank) & rank_mask) != rank_mask) return 1;
+    if (target < m) return 0; // distributed.cpp:161-165
+    const int rank_bit = target - m;
+    *peer = rank ^ (1 << rank_bit);                  // distributed.cpp:50-57
+    *own_lo = ((rank >> rank_bit) & 1) == 0 ? 1 : 0; // distributed.cpp:169
+    return 2;
+}
+
+// ---------------------------------------------------------------- register
+
+QuregImpl* create_register(Env* env, int N, bool density) {
+    if (N < 1)
+        throw DomainError("register needs at least 1 qubit, got " + std::to_string(N));
+    const int flat = density ? 2 * N : N;
+    // register.cpp:106-117: preflight the byte count.
+    if (flat + 4 > 63)
+        throw ResourceError("register of " + std::to_string(N) + " qubits requires 2^" +
+                            std::to_string(flat + 4) + " bytes");
+    if (env->rank_log2 > flat)
+        throw DomainError("rank count 2^" + std::to_string(env->rank_log2) + " invalid for " +
+                          std::to_string(flat) + " qubits (need 0 <= k <= n)");
+    if (density && env->rank_log2 > N)
+        throw DomainError("density matrix of " + std::to_string(N) +
+                          " qubits cannot be split over 2^" + std::to_string(env->rank_log2) +
+                          " ranks (need k <= N)");
+    auto q = std::make_unique<QuregImpl>();
+    q->env = env;
+    q->N = N;
+    q->flat = flat;
+    q->density = density;
+    q->local_qubits = flat - env->rank_log2;
+    q->local_len = uint64_t{1} << q->local_qubits;
+    const int nshards = env->mode == Mode::Loopback ? env->num_ranks : 1;
+    const size_t bytes = q->local_len * sizeof(double2);
+    for (int s = 0; s < nshards; ++s) {
+        Shard sh;
+        sh.rank = env->mode == Mode::Loopback ? s : env->rank;
+        if (cudaMalloc(&sh.amps, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            throw ResourceError("failed to allocate " + std::to_string(bytes) +
+                                " bytes of amplitude storage");
+        }
+        q->shards.push_back(sh);
+    }
+    const int nresults = std::max(nshards, env->num_ranks) + 1;
+    if (cudaMalloc(&q->partials, kReduceBlocks * sizeof(double2)) != cudaSuccess ||
+        cudaMalloc(&q->results, nresults * sizeof(double2)) != cudaSuccess) {
+        cudaGetLastError();
+        throw ResourceError("failed to allocate reduction scratch");
+    }
+    q->fill_zero();
+    if (q->shards[0].rank == 0) {
+        const double2 one = make_double2(1.0, 0.0);
+        cuda_check(cudaMemcpyAsync(q->shards[0].amps, &one, sizeof(one), cudaMemcpyHostToDevice,
+                                   env->stream),
+                   "init zero state");
+        cuda_check(cudaStreamSynchronize(env->stream), "init zero state");
+    }
+    env->quregs.insert(q.get());
+    return q.release();
+}
+
+QuregImpl::~QuregImpl() {
+    if (env) {
+        cudaStreamSynchronize(env->stream);
+        env->quregs.erase(this);
+    }
+    for (auto& s : shards) cudaFree(s.amps);
+    cudaFree(recv[0]);
+    cudaFree(recv[1]);
+    cudaFree(partials);
+    cudaFree(results);
+}
+
+void QuregImpl::fill_zero() {
+    discard();
+    for (auto& s : shards)
+        cuda_check(cudaMemsetAsync(s.amps, 0, local_len * sizeof(double2), env->stream),
+                   "cudaMemsetAsync");
+}
+
+void QuregImpl::ensure_recv(uint64_t len) {
+    if (recv_len >= len) return;
+    cuda_check(cudaStreamSynchronize(env->stream), "sync");
+    cudaFree(recv[0]);
+    cudaFree(recv[1]);
+    recv[0] = recv[1] = nullptr;
+    recv_len = 0;
+    if (cudaMalloc(&recv[0], len * sizeof(double2)) != cudaSuccess ||
+        cudaMalloc(&recv[1], len * sizeof(double2)) != cudaSuccess) {
+        cudaGetLastError();
+        throw ResourceError("failed to allocate " + std::to_string(2 * len * sizeof(double2)) +
+                            " bytes of exchange buffers");
+    }
+    recv_len = len;
+}
+
+int QuregImpl::pass_H() const {
+    const int h = std::min(env->reg_qubits, local_qubits - kLaneQubits);
+    return h < 1 ? 0 : h;
+}
+
+// -------------------------------------------------------------- scheduling
+
+void QuregImpl::enqueue(const FlatOp& op) {
+    const bool pair = op.kind == FK_GATE && op.cls != CLS_DIAG;
+    if (op.kind == FK_DEPOL) {
+        flush();
+        run_depol(op);
+        return;
+    }
+    if (pair && op.q0 >= local_qubits) {
+        flush();
+        run_exchange_gate(op);
+        return;
+    }
+    if (env->fusion_mode == 2 || pass_H() < 1) {
+        flush();
+        run_simple(op);
+        ++passes;
+        return;
+    }
+    if (pair && op.q0 >= kLaneQubits &&
+        std::find(regs.begin(), regs.end(), op.q0) == regs.end()) {
+        if (static_cast<int>(regs.size()) >= pass_H()) flush();
+        regs.push_back(op.q0);
+    }
+    pending.push_back(op);
+    if (env->fusion_mode == 1 || static_cast<int>(pending.size()) >= env->max_ops) flush();
+}
+
+void QuregImpl::flush() {
+    if (pending.empty()) {
+        regs.clear();
+        return;
+    }
+    launch_fused();
+    pending.clear();
+    regs.clear();
+}
+
+void QuregImpl::launch_fused() {
+    const int H = pass_H();
+    std::vector<int> r = regs;
+    for (int q = local_qubits - 1; static_cast<int>(r.size()) < H && q >= kLaneQubits; --q)
+        if (std::find(r.begin(), r.end(), q) == r.end()) r.push_back(q);
+    std::sort(r.begin(), r.end());
+
+    PassParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.num_tiles = uint64_t{1} << (local_qubits - kLaneQubits - H);
+    P.H = H;
+    P.num_ops = static_cast<int>(pending.size());
+    uint64_t reg_bits = 0;
+    for (int j = 0; j < H; ++j) {
+        P.reg_pos[j] = r[j];
+        reg_bits |= uint64_t{1} << r[j];
+    }
+    for (int i = 0; i < (1 << H); ++i) {
+        uint64_t off = 0;
+        for (int j = 0; j < H; ++j)
+            if ((i >> j) & 1) off |= uint64_t{1} << r[j];
+        P.reg_off[i] = off;
+    }
+    auto loc = [&](int q) -> QubitLoc {
+        if (q < 0) return QubitLoc{LOC_OUTER, 0};
+        if (q < kLaneQubits) return QubitLoc{LOC_LANE, static_cast<uint8_t>(q)};
+        for (int j = 0; j < H; ++j)
+            if (r[j] == q) return QubitLoc{LOC_REG, static_cast<uint8_t>(j)};
+        return QubitLoc{LOC_OUTER, static_cast<uint8_t>(q)};
+    };
+    for (size_t k = 0; k < pending.size(); ++k) {
+        const FlatOp& op = pending[k];
+        PassOp& po = P.ops[k];
+        switch (op.kind) {
+        case FK_GATE:
+            po.kind = op.cls == CLS_DIAG ? PO_DIAG
+                                         : (op.q0 < kLaneQubits ? PO_PAIR_LANE : PO_PAIR_REG);
+            break;
+        case FK_DEPHASE: po.kind = PO_DEPHASE; break;
+        default: po.kind = PO_COLLAPSE; break;
+        }
+        po.cls = op.cls;
+        po.flags = op.kind == FK_COLLAPSE ? (op.q1 >= 0 ? 1 : 0) : op.flags;
+        po.outcome = op.outcome;
+        po.q0 = loc(op.q0);
+        po.q1 = loc(op.q1);
+        po.lane_cmask = static_cast<uint32_t>(op.cmask & ((1u << kLaneQubits) - 1));
+        po.reg_cmask = 0;
+        for (int j = 0; j < H; ++j)
+            if ((op.cmask >> r[j]) & 1) po.reg_cmask |= 1u << j;
+        po.outer_cmask = op.cmask & ~uint64_t{(1u << kLaneQubits) - 1} & ~reg_bits;
+        std::memcpy(po.m, op.m, sizeof(po.m));
+    }
+    ProfScope prof(env, PK_PASS);
+    for (auto& s : shards) {
+        P.global_offset = goff(s);
+        launch_pass(s.amps, P, env->stream);
+    }
+    cuda_check(cudaGetLastError(), "fused pass launch");
+    ++passes;
+}
+
+void QuregImpl::run_simple(const FlatOp& op) {
+    ProfScope prof(env, PK_SIMPLE);
+    for (auto& s : shards) {
+        switch (op.kind) {
+        case FK_GATE:
+            if (op.cls == CLS_DIAG) {
+                Mat2 m;
+                std::memcpy(m.m, op.m, sizeof(m.m));
+                launch_diag_simple(s.amps, local_len, goff(s), op.q0, op.cmask, m, op.flags,
+                                   env->stream);
+            } else {
+                const uint64_t rank_mask = op.cmask >> local_qubits;
+                if ((static_cast<uint64_t>(s.rank) & rank_mask) != rank_mask) break;
+                Mat2 m;
+                std::memcpy(m.m, op.m, sizeof(m.m));
+                launch_gate_simple(s.amps, local_qubits, op.q0, op.cmask & (local_len - 1), m,
+                                   op.cls, env->stream);
+            }
+            break;
+        case FK_DEPHASE:
+            launch_dephase(s.amps, local_len, goff(s), op.q0, op.q1, op.m[0], env->stream);
+            break;
+        case FK_COLLAPSE:
+            launch_collapse(s.amps, local_len, goff(s), op.q0, op.q1, op.outcome, op.m[0],
+                            env->stream);
+            break;
+        default: break;
+        }
+    }
+    cuda_check(cudaGetLastError(), "kernel launch");
+}
+
+// ---------------------------------------------------------------- exchange
+
+namespace {
+
+struct ExchangeEvents {
+    cudaEvent_t start = nullptr, recv[2] = {nullptr, nullptr}, done[2] = {nullptr, nullptr};
+    explicit ExchangeEvents() {
+        cudaEventCreateWithFlags(&start, cudaEventDisableTiming);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventCreateWithFlags(&recv[i], cudaEventDisableTiming);
+            cudaEventCreateWithFlags(&done[i], cudaEventDisableTiming);
+        }
+    }
+    ~ExchangeEvents() {
+        cudaEventDestroy(start);
+        for (int i = 0; i < 2; ++i) {
+            cudaEventDestroy(recv[i]);
+            cudaEventDestroy(done[i]);
+        }
+    }
+};
+
+} // namespace
+
+// Pairwise sub-chunked exchange + combine. `combine(shard, chunk_ptr,
+// recv_ptr, len, idx0)` writes only the shard's own half
+// (distributed.cpp:174-187); chunk j is sent before combine(j) overwrites it
+// (the in-place ordering rule of the PerAmplitude strategy, :215-231).
+template <class Combine>
+static void exchange_rounds(QuregImpl& q, int rank_bit, uint64_t rank_mask, uint64_t chunk,
+                            Combine&& combine) {
+    Env* env = q.env;
+    const uint64_t bytes = chunk * sizeof(double2);
+    if (env->mode == Mode::Nccl) {
+        Shard& s = q.shards[0];
+        if ((static_cast<uint64_t>(s.rank) & rank_mask) != rank_mask) return;
+        const int peer = s.rank ^ (1 << rank_bit);
+        ExchangeEvents ev;
+        cuda_check(cudaEventRecord(ev.start, env->stream), "event");
+        cuda_check(cudaStreamWaitEvent(env->comm_stream, ev.start, 0), "event");
+        uint64_t j = 0;
+        for (uint64_t c0 = 0; c0 < q.local_len; c0 += chunk, ++j) {
+            const int b = static_cast<int>(j & 1);
+            if (j >= 2) cuda_check(cudaStreamWaitEvent(env->comm_stream, ev.done[b], 0), "event");
+            env->nccl->sendrecv(peer, s.amps + c0, q.recv[b], bytes, env->comm_stream);
+            cuda_check(cudaEventRecord(ev.recv[b], env->comm_stream), "event");
+            cuda_check(cudaStreamWaitEvent(env->stream, ev.recv[b], 0), "event");
+            combine(s, s.amps + c0, q.recv[b], chunk, c0);
+            cuda_check(cudaEventRecord(ev.done[b], env->stream), "event");
+            s.messages += 1;
+            s.bytes += bytes;
+        }
+        // events are destroyed after the stream consumed them (the runtime
+        // defers destruction of recorded events).
+        return;
+    }
+    // Loopback: 2^k virtual ranks on this device; each pair's cell copies both
+    // directions (InProcessTransport::exchange, transport.cpp:39-50).
+    for (auto& s : q.shards) {
+        const int peer = s.rank ^ (1 << rank_bit);
+        if (peer < s.rank) continue;
+        if ((static_cast<uint64_t>(s.rank) & rank_mask) != rank_mask) continue;
+        Shard& p = q.shards[peer];
+        for (uint64_t c0 = 0; c0 < q.local_len; c0 += chunk) {
+            cuda_check(cudaMemcpyAsync(q.recv[0], p.amps + c0, bytes, cudaMemcpyDeviceToDevice,
+                                       env->stream),
+                       "loopback exchange");
+            cuda_check(cudaMemcpyAsync(q.recv[1], s.amps + c0, bytes, cudaMemcpyDeviceToDevice,
+                                       env->stream),
+                       "loopback exchange");
+            combine(s, s.amps + c0, q.recv[0], chunk, c0);
+            combine(p, p.amps + c0, q.recv[1], chunk, c0);
+            s.messages += 1;
+            s.bytes += bytes;
+            p.messages += 1;
+            p.bytes += bytes;
+        }
+    }
+}
+
+void QuregImpl::run_exchange_gate(const FlatOp& op) {
+    const int rank_bit = op.q0 - local_qubits;
+    const uint64_t rank_mask = op.cmask >> local_qubits;
+    const uint64_t low_mask = op.cmask & (local_len - 1);
+    const uint64_t chunk = std::min<uint64_t>(env->chunk_amps, local_len);
+    ensure_recv(chunk);
+    Mat2 m;
+    std::memcpy(m.m, op.m, sizeof(m.m));
+    ProfScope prof(env, PK_EXCHANGE);
+    exchange_rounds(*this, rank_bit, rank_mask, chunk,
+                    [&](Shard& s, double2* mine, double2* theirs, uint64_t len, uint64_t idx0) {
+                        const int own_lo = ((s.rank >> rank_bit) & 1) == 0;
+                        launch_combine(mine, theirs, len, idx0, low_mask, own_lo, m, op.cls,
+                                       env->stream);
+                    });
+    cuda_check(cudaGetLastError(), "exchange combine");
+    ++passes;
+}
+
+void QuregImpl::run_depol(const FlatOp& op) {
+    const double keep = op.m[0], swap = op.m[1], off = op.m[2];
+    ProfScope prof(env, PK_DEPOL);
+    if (op.q1 < local_qubits) {
+        for (auto& s : shards)
+            launch_depolarise(s.amps, local_qubits, op.q0, op.q1, keep, swap, off, env->stream);
+        cuda_check(cudaGetLastError(), "depolarise");
+        ++passes;
+        return;
+    }
+    const int rank_bit = op.q1 - local_qubits;
+    uint64_t chunk = std::min<uint64_t>(env->chunk_amps, local_len);
+    chunk = std::max<uint64_t>(chunk, uint64_t{2} << op.q0);
+    ensure_recv(chunk);
+    exchange_rounds(*this, rank_bit, 0, chunk,
+                    [&](Shard& s, double2* mine, double2* theirs, uint64_t len, uint64_t idx0) {
+                        const int own_col = (s.rank >> rank_bit) & 1;
+                        launch_combine_depol(mine, theirs, len, idx0, op.q0, own_col, keep, swap,
+                                             off, env->stream);
+                    });
+    cuda_check(cudaGetLastError(), "depolarise exchange");
+    ++passes;
+}
+
+// -------------------------------------------------------------- reductions
+
+namespace {
+struct HostDD {
+    double hi = 0.0, lo = 0.0;
+    void add(double xh, double xl) {
+        const double s = hi + xh;
+        const double bb = s - hi;
+        const double e = (hi - (s - bb)) + (xh - bb);
+        const double t = e + lo + xl;
+        hi = s + t;
+        lo = t - (hi - s);
+    }
+};
+} // namespace
+
+double QuregImpl::combine_results(int n) {
+    std::vector<double2> host(std::max(n, env->num_ranks));
+    if (env->mode == Mode::Nccl && env->num_ranks > 1) {
+        env->nccl->allgather(results, results + 1, sizeof(double2), env->stream);
+        cuda_check(cudaMemcpyAsync(host.data(), results + 1, env->num_ranks * sizeof(double2),
+                                   cudaMemcpyDeviceToHost, env->stream),
+                   "reduction readback");
+        n = env->num_ranks;
+    } else {
+        cuda_check(cudaMemcpyAsync(host.data(), results, n * sizeof(double2),
+                                   cudaMemcpyDeviceToHost, env->stream),
+                   "reduction readback");
+    }
+    cuda_check(cudaStreamSynchronize(env->stream), "reduction");
+    HostDD acc;
+    for (int i = 0; i < n; ++i) acc.add(host[i].x, host[i].y); // rank order
+    return acc.hi + acc.lo;
+}
+
+double QuregImpl::reduce_norm(int t, int outcome) {
+    flush();
+    ProfScope prof(env, PK_REDUCE);
+    for (size_t k = 0; k < shards.size(); ++k)
+        launch_reduce_norm(shards[k].amps, local_len, goff(shards[k]), t, outcome, partials,
+                           results + k, env->stream);
+    cuda_check(cudaGetLastError(), "reduce");
+    return combine_results(static_cast<int>(shards.size()));
+}
+
+double QuregImpl::reduce_diag(int t, int outcome, int comp) {
+    flush();
+    ProfScope prof(env, PK_REDUCE);
+    for (size_t k = 0; k < shards.size(); ++k)
+        launch_reduce_diag(shards[k].amps, local_len, goff(shards[k]), N, t, outcome, comp,
+                           partials, results + k, env->stream);
+    cuda_check(cudaGetLastError(), "reduce");
+    return combine_results(static_cast<int>(shards.size()));
+}
+
+Complex QuregImpl::trace() {
+    // density.cpp:147-154 sums both parts of the diagonal.
+    Complex c;
+    c.real = reduce_diag(-1, 0, 0);
+    c.imag = reduce_diag(-1, 0, 1);
+    return c;
+}
+
+void QuregImpl::get_flat(uint64_t start, uint64_t num, double2* out) {
+    flush();
+    const uint64_t end = start + num;
+    if (env->mode == Mode::Nccl && env->num_ranks > 1) {
+        if (num != 1) {
+            const uint64_t lo = goff(shards[0]), hi = lo + local_len;
+            if (start < lo || end > hi)
+                throw DomainError("bulk reads are limited to this rank's amplitudes [" +
+                                  std::to_string(lo) + ", " + std::to_string(hi) + ")");
+            cuda_check(cudaMemcpyAsync(out, shards[0].amps + (start - lo), num * sizeof(double2),
+                                       cudaMemcpyDeviceToHost, env->stream),
+                       "read");
+            cuda_check(cudaStreamSynchronize(env->stream), "read");
+            return;
+        }
+        // single amplitude: the owner contributes it, everyone gets it.
+        const uint64_t lo = goff(shards[0]);
+        const int owner = static_cast<int>(start >> local_qubits);
+        double2 zero = make_double2(0.0, 0.0);
+        if (owner == shards[0].rank)
+            cuda_check(cudaMemcpyAsync(results, shards[0].amps + (start - lo), sizeof(double2),
+                                       cudaMemcpyDeviceToDevice, env->stream),
+                       "read");
+        else
+            cuda_check(cudaMemcpyAsync(results, &zero, sizeof(double2), cudaMemcpyHostToDevice,
+                                       env->stream),
+                       "read");
+        env->nccl->allgather(results, results + 1, sizeof(double2), env->stream);
+        cuda_check(cudaMemcpyAsync(out, results + 1 + owner, sizeof(double2),
+                                   cudaMemcpyDeviceToHost, env->stream),
+                   "read");
+        cuda_check(cudaStreamSynchronize(env->stream), "read");
+        return;
+    }
+    for (auto& s : shards) {
+        const uint64_t lo = goff(s), hi = lo + local_len;
+        const uint64_t a = std::max(lo, start), b = std::min(hi, end);
+        if (a >= b) continue;
+        cuda_check(cudaMemcpyAsync(out + (a - start), s.amps + (a - lo), (b - a) * sizeof(double2),
+                                   cudaMemcpyDeviceToHost, env->stream),
+                   "read");
+    }
+    cuda_check(cudaStreamSynchronize(env->stream), "read");
+}
+
+void QuregImpl::set_flat(uint64_t start, uint64_t num, const double2* in) {
+    flush();
+    const uint64_t end = start + num;
+    for (auto& s : shards) {
+        const uint64_t lo = goff(s), hi = lo + local_len;
+        const uint64_t a = std::max(lo, start), b = std::min(hi, end);
+        if (a >= b) continue;
+        cuda_check(cudaMemcpyAsync(s.amps + (a - lo), in + (a - start), (b - a) * sizeof(double2),
+                                   cudaMemcpyHostToDevice, env->stream),
+                   "write");
+    }
+    cuda_check(cudaStreamSynchronize(env->stream), "write");
+}
+
+} // namespace qgpu

@@ -1,0 +1,154 @@
+// runtime.h — host runtime of libqgpu: environment (device, streams,
+// transport, RNG), registers (HBM shards), the op queue that fuses gates into
+// HBM passes, the distributed exchange engine and the reductions.
+#pragma once
+
+#include "QuEST.h"
+#include "qgpu.h"
+#include "qgpu_device.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <set>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+namespace qgpu {
+
+// Exceptions stay inside the library; api.cpp converts them to the error
+// handler + codes (the reference's exception classes, types.hpp:31-55).
+struct DomainError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct ResourceError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct CommError : std::runtime_error { using std::runtime_error::runtime_error; };
+struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
+
+void cuda_check(cudaError_t e, const char* what);
+
+// ------------------------------------------------------------- transport
+
+class NcclComm; // transport.cpp
+
+enum class Mode { Single, Loopback, Nccl };
+
+struct Env {
+    int device = 0;
+    cudaStream_t stream = nullptr;      // all compute
+    cudaStream_t comm_stream = nullptr; // NCCL sends/recvs
+    Mode mode = Mode::Single;
+    int rank = 0;        // this process's rank (Nccl) or 0
+    int num_ranks = 1;   // total ranks (virtual ranks in Loopback)
+    int rank_log2 = 0;
+    uint64_t rng = 0;    // SplitMix64 state for measure()
+    int fusion_mode = 0; // 0 fused, 1 one pass per op, 2 simple per-op kernels
+    int max_ops = kMaxPassOps;
+    int reg_qubits = 4;
+    uint64_t chunk_amps = uint64_t{1} << 24;
+    std::unique_ptr<NcclComm> nccl;
+    std::set<struct QuregImpl*> quregs;
+
+    // Launch profiling (qgpuProfileStart/Stop): an event pair around every
+    // launch of the hot kernels, on the stream they run on.
+    bool profile = false;
+    struct ProfRec {
+        cudaEvent_t start, stop;
+        int kind;
+    };
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> event_pool;
+    cudaEvent_t take_event();
+
+    ~Env();
+};
+
+enum ProfKind { PK_PASS = 0, PK_SIMPLE = 1, PK_EXCHANGE = 2, PK_DEPOL = 3, PK_REDUCE = 4 };
+
+// Brackets the enclosed launches with an event pair when profiling is on.
+class ProfScope {
+  public:
+    ProfScope(Env* env, int kind);
+    ~ProfScope();
+
+  private:
+    Env* env_;
+    int kind_;
+    cudaEvent_t start_ = nullptr;
+};
+
+// --------------------------------------------------------------- registers
+
+enum FlatKind : uint8_t { FK_GATE = 0, FK_DEPHASE = 1, FK_DEPOL = 2, FK_COLLAPSE = 3 };
+
+// An operation on the flat 2^flat vector (the reference's FlatGateOp,
+// distributed.hpp:78-85, extended with the channels and collapse).
+struct FlatOp {
+    uint8_t kind = FK_GATE;
+    uint8_t cls = CLS_GENERIC;
+    uint8_t flags = 0;
+    uint8_t outcome = 0;
+    int q0 = 0, q1 = -1;
+    uint64_t cmask = 0;
+    double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+};
+
+uint8_t classify(const double* m, uint8_t* diag_flags);
+
+struct Shard {
+    int rank = 0;
+    double2* amps = nullptr;
+    uint64_t messages = 0, bytes = 0; // CommStats per rank
+};
+
+struct QuregImpl {
+    Env* env = nullptr;
+    int N = 0;          // qubits represented
+    int flat = 0;       // N (SV) or 2N (DM)
+    bool density = false;
+    int local_qubits = 0;
+    uint64_t local_len = 0;
+    std::vector<Shard> shards; // 1, or 2^k virtual ranks (Loopback)
+    double2* recv[2] = {nullptr, nullptr};
+    uint64_t recv_len = 0;
+    double2* partials = nullptr; // reduction scratch
+    double2* results = nullptr;  // one (hi, lo) per shard
+    uint64_t passes = 0;
+
+    // the open pass
+    std::vector<FlatOp> pending;
+    std::vector<int> regs;
+
+    ~QuregImpl();
+
+    void enqueue(const FlatOp& op);
+    void flush();
+    void discard() { pending.clear(); regs.clear(); }
+
+    // reductions (flush first; synchronous)
+    double reduce_norm(int t, int outcome); // sum |a|^2 (t < 0: all)
+    double reduce_diag(int t, int outcome, int comp = 0); // sum Re (comp 0) / Im (1) rho_jj
+    Complex trace();
+
+    void get_flat(uint64_t start, uint64_t num, double2* out);
+    void set_flat(uint64_t start, uint64_t num, const double2* in);
+    void fill_zero();
+
+  private:
+    int pass_H() const;
+    void run_simple(const FlatOp& op);
+    void launch_fused();
+    void run_exchange_gate(const FlatOp& op);
+    void run_depol(const FlatOp& op);
+    void ensure_recv(uint64_t len);
+    uint64_t goff(const Shard& s) const { return static_cast<uint64_t>(s.rank) * local_len; }
+    double combine_results(int n); // rank-ordered double-double sum
+};
+
+QuregImpl* create_register(Env* env, int N, bool density);
+
+// Pure planner (qgpu.h: qgpuPlanGate).
+int plan_gate(int flat, int rank_log2, int rank, int target, uint64_t cmask, int* peer,
+              int* own_lo, uint64_t* low_mask);
+
+} // namespace qgpu

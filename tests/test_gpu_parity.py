@@ -1,0 +1,290 @@
+"""Parity of the CUDA product (through the C-ABI) with the CPU checkers.
+
+Bar: bit-identical amplitudes (np.array_equal, i.e. up to the sign of zero)
+for every gate / channel path, since the kernels evaluate the reference's own
+fma chain; reductions within 1e-12 (compensated sums in a different order).
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+from paper_1802_08032_b200 import circuits as C
+from paper_1802_08032_b200 import quest
+from tests.harness import bits_equal, oracle_run, random_gate_circuit, to_oracle_ops
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def env():
+    e = quest.Env()
+    yield e
+    e.destroy()
+
+
+def run_product(env, circuit, density=False, init=None):
+    q = quest.QuregHandle(env, circuit.num_qubits, density)
+    try:
+        if init is not None:
+            q.set_state(init)
+        C.apply_circuit(q, circuit)
+        return q.state()
+    finally:
+        q.destroy()
+
+
+def assert_parity(got, want):
+    err = float(np.max(np.abs(got - want))) if got.size else 0.0
+    assert err <= TOL, f"max-abs error {err}"
+    assert bits_equal(got, want), f"not bit-identical (max-abs {err})"
+
+
+FUSION = [(0, 48, 4), (0, 48, 3), (0, 48, 5), (0, 7, 2), (1, 0, 4), (2, 0, 0)]
+
+
+@pytest.mark.parametrize("mode,max_ops,h", FUSION)
+@pytest.mark.parametrize("n", [4, 7, 12])
+def test_random_gates_all_fusion_modes(env, mode, max_ops, h, n):
+    env.set_fusion(mode, max_ops if max_ops else 48, h if h else 4)
+    try:
+        c = random_gate_circuit(n, 150, seed=n * 31 + mode, max_controls=3)
+        assert_parity(run_product(env, c), oracle_run(c))
+    finally:
+        env.set_fusion(0, 48, 4)
+
+
+@pytest.mark.parametrize("n", [6, 11, 16])
+def test_random_gates_from_random_state(env, n):
+    rng = np.random.default_rng(n)
+    init = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+    c = random_gate_circuit(n, 200, seed=7 + n, max_controls=4)
+    assert_parity(run_product(env, c, init=init), oracle_run(c, init=init))
+
+
+def test_layered_circuit_c1_against_reference(env):
+    """Config C1: 20 qubits, depth 20, seed 12345, vs the compiled reference."""
+    c = C.layered_random_circuit(20, 20, 12345)
+    want = oracle.ref_run(20, to_oracle_ops(c), workers=8) if oracle.ref_available() else oracle_run(c)
+    assert_parity(run_product(env, c), want)
+
+
+def test_reference_generator_circuit(env):
+    c = C.reference_random_circuit(18, 30, 2)
+    assert_parity(run_product(env, c), oracle_run(c))
+
+
+@pytest.mark.parametrize("mode", [0, 1, 2])
+@pytest.mark.parametrize("N", [2, 4, 6])
+def test_density_matrix_with_channels(env, mode, N):
+    env.set_fusion(mode, 48, 4)
+    try:
+        c = random_gate_circuit(N, 120, seed=500 + N, max_controls=2, channels=True)
+        assert_parity(run_product(env, c, density=True), oracle_run(c, density=True))
+    finally:
+        env.set_fusion(0, 48, 4)
+
+
+def test_density_c4_noisy_layered(env):
+    c = C.layered_random_circuit(7, 6, 99, noise_pmax=0.1)
+    assert_parity(run_product(env, c, density=True), oracle_run(c, density=True))
+
+
+@pytest.mark.parametrize("n", [5, 9, 14])
+def test_every_target_and_control_placement(env, n):
+    """Per-target sweep (SURVEY.md §8(d) C2 sweep) over every stride, with
+    controls below / above the target."""
+    c = C.Circuit(n, 0, [])
+    rng = np.random.default_rng(n)
+    for t in range(n):
+        for name in ("H", "RX", "RY", "RZ", "PHASE", "X", "SX"):
+            c.ops.append(C.GateOp(name, t, (), angle=float(rng.uniform(0, 6))))
+        for cq in range(n):
+            if cq != t:
+                c.ops.append(C.GateOp("X", t, (cq,)))
+                c.ops.append(C.GateOp("PHASE", t, (cq,), angle=float(rng.uniform(0, 6))))
+    assert_parity(run_product(env, c), oracle_run(c))
+
+
+def test_reductions(env):
+    n = 13
+    c = random_gate_circuit(n, 80, seed=3)
+    want = oracle_run(c)
+    q = quest.QuregHandle(env, n)
+    C.apply_circuit(q, c)
+    assert abs(q.calcTotalProb() - oracle.orc_norm_kahan(want)) < TOL
+    for t in range(n):
+        for o in (0, 1):
+            assert abs(q.calcProbOfOutcome(t, o) - oracle.orc_prob_of_outcome(want, n, t, o)) < TOL
+    q.destroy()
+    N = 4
+    c = random_gate_circuit(N, 60, seed=4, channels=True)
+    want = oracle_run(c, density=True)
+    q = quest.QuregHandle(env, N, density=True)
+    C.apply_circuit(q, c)
+    assert abs(q.calcTotalProb() - oracle.orc_trace(want, N).real) < TOL
+    assert abs(q.calcPurity() - oracle.orc_norm_kahan(want)) < TOL
+    for t in range(N):
+        assert abs(q.calcProbOfOutcome(t, 1) - oracle.orc_prob_of_outcome(want, N, t, 1, density=True)) < TOL
+    tr = quest.call("qgpuTrace", q.h)
+    assert abs(complex(tr.real, tr.imag) - oracle.orc_trace(want, N)) < TOL
+    q.destroy()
+
+
+@pytest.mark.parametrize("density", [False, True])
+def test_collapse_and_measure_match_restatement(env, density):
+    n = 5 if density else 10
+    c = random_gate_circuit(n, 60, seed=11)
+    amps = oracle_run(c, density=density)
+    q = quest.QuregHandle(env, n, density)
+    C.apply_circuit(q, c)
+    p = q.collapseToOutcome(2, 1)
+    want_p = oracle.orc_prob_of_outcome(amps, n, 2, 1, density)
+    assert abs(p - want_p) < TOL
+    amps = oracle.orc_collapse(amps, n, 2, 1, p, density)
+    got = q.state()
+    assert np.max(np.abs(got - amps)) < TOL
+    # measurement outcomes under a fixed seed match the restatement exactly
+    env.seed(12345)
+    st = oracle.orc_seed([12345])
+    for t in (0, 3, 4):
+        o = q.measure(t)
+        ow, pw, amps, st = oracle.orc_measure(amps, n, t, st, density)
+        assert o == ow
+    assert np.max(np.abs(q.state() - amps)) < TOL
+    q.destroy()
+
+
+def test_qft_probabilities(env):
+    """C5 analytic KAT: P(outcome) = 1/2 on every qubit after QFT of |x>."""
+    n = 16
+    q = quest.QuregHandle(env, n)
+    q.initClassicalState(12345)
+    C.apply_circuit(q, C.qft_circuit(n, mcpf_every=3))
+    for t in range(n):
+        assert abs(q.calcProbOfOutcome(t, 0) - 0.5) < TOL
+    assert abs(q.calcTotalProb() - 1.0) < TOL
+    q.destroy()
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+@pytest.mark.parametrize("density", [False, True])
+def test_loopback_distributed_equals_single(k, density):
+    """2^k virtual ranks on one GPU through the sub-chunked exchange protocol
+    == the single-rank result (acceptance 3)."""
+    n = 4 if density else 11
+    c = random_gate_circuit(n, 120, seed=40 + k, max_controls=2, channels=density)
+    want = oracle_run(c, density=density)
+    env = quest.Env.loopback(1 << k)
+    env.set_exchange_chunk(16)
+    try:
+        got = run_product(env, c, density=density)
+        assert_parity(got, want)
+        q = quest.QuregHandle(env, n, density)
+        C.apply_circuit(q, c)
+        assert abs(q.calcTotalProb() - (oracle.orc_trace(want, n).real if density else oracle.orc_norm_kahan(want))) < TOL
+        q.destroy()
+    finally:
+        env.destroy()
+
+
+def test_loopback_comm_accounting():
+    """Exchange accounting: a communicated gate moves exactly
+    16 * 2^(n-k) bytes per rank, in 2^(n-k)/chunk messages; local gates none."""
+    n, k = 10, 2
+    env = quest.Env.loopback(1 << k)
+    env.set_exchange_chunk(64)
+    q = quest.QuregHandle(env, n)
+    q.hadamard(3)
+    q.flush()
+    assert q.comm_stats(4)[1].sum() == 0
+    q.hadamard(9)
+    q.flush()
+    msgs, byts = q.comm_stats(4)
+    assert list(byts) == [16 * (1 << (n - k))] * 4
+    assert list(msgs) == [(1 << (n - k)) // 64] * 4
+    q.controlledNot(9, 8)  # control on rank bit 1: ranks 0, 1 skip
+    q.flush()
+    msgs2, byts2 = q.comm_stats(4)
+    assert list(byts2 - byts) == [0, 0, 16 * 256, 16 * 256]
+    q.destroy()
+    env.destroy()
+
+
+def test_validation_before_mutation(env):
+    q = quest.QuregHandle(env, 5)
+    q.hadamard(0)
+    before = q.state()
+    with pytest.raises(quest.DomainError, match="invalid target qubit 5"):
+        q.hadamard(5)
+    with pytest.raises(quest.DomainError, match="overlaps the target"):
+        q.controlledNot(2, 2)
+    arr, k = quest.int_array([1, 1, 3])
+    with pytest.raises(quest.DomainError, match="duplicate control"):
+        q.multiControlledPhaseFlip(arr, k)
+    with pytest.raises(quest.DomainError, match="not unitary"):
+        q.unitary(0, quest.cmatrix2([1, 0, 1, 0, 0, 0, 1, 0]))
+    with pytest.raises(quest.DomainError, match="density-matrix"):
+        q.mixDephasing(0, 0.1)
+    with pytest.raises(quest.DomainError, match="finite"):
+        q.set_state(np.array([np.nan + 0j]))
+    with pytest.raises(quest.DomainError, match="out of range"):
+        q.getAmp(32)
+    assert bits_equal(q.state(), before)
+    q.destroy()
+    d = quest.QuregHandle(env, 2, density=True)
+    with pytest.raises(quest.DomainError, match=r"\[0, 1/2\]"):
+        d.mixDephasing(0, 0.6)
+    with pytest.raises(quest.DomainError, match=r"\[0, 3/4\]"):
+        d.mixDepolarising(1, 0.8)
+    with pytest.raises(quest.DomainError, match="density matrix"):
+        d.hadamard(2)
+    d.destroy()
+
+
+def test_init_and_amplitude_access(env):
+    q = quest.QuregHandle(env, 6)
+    q.initPlusState()
+    assert abs(q.getAmp(17).real - 1 / 8) < 1e-15
+    q.initClassicalState(5)
+    assert q.getAmp(5).real == 1.0 and q.calcTotalProb() == 1.0
+    rng = np.random.default_rng(1)
+    a = rng.normal(size=64) + 1j * rng.normal(size=64)
+    q.set_state(a)
+    assert bits_equal(q.state(), a)
+    q.initZeroState()
+    assert q.getAmp(0).real == 1.0 and q.getProbAmp(1) == 0.0
+    q.destroy()
+    d = quest.QuregHandle(env, 3, density=True)
+    d.initPlusState()
+    assert abs(quest.call("getDensityAmp", d.h, 2, 5).real - 1 / 8) < 1e-15
+    assert abs(d.calcTotalProb() - 1.0) < 1e-14
+    d.destroy()
+
+
+def test_kernels_actually_launch(env):
+    before = quest.kernel_launches()
+    q = quest.QuregHandle(env, 12)
+    C.apply_circuit(q, C.layered_random_circuit(12, 4, 1))
+    q.calcTotalProb()
+    assert quest.kernel_launches() > before
+    q.destroy()
+
+
+@pytest.mark.slow
+def test_30q_forward_inverse_property(env):
+    """Config C2 size: layered 30-qubit circuit then its inverse returns |0>
+    (size-independent property), and the norm stays 1."""
+    n = 30
+    c = C.layered_random_circuit(n, 4, 12345)
+    q = quest.QuregHandle(env, n)
+    C.apply_circuit(q, c)
+    assert abs(q.calcTotalProb() - 1.0) < 1e-12
+    C.apply_circuit(q, C.inverse_circuit(c))
+    a0 = q.getAmp(0)
+    assert abs(a0.real - 1.0) < 1e-12 and abs(a0.imag) < 1e-12
+    assert abs(q.calcProbOfOutcome(n - 1, 0) - 1.0) < 1e-12
+    q.destroy()
