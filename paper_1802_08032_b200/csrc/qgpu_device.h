@@ -77,4 +77,57 @@ struct Mat2 {
     double m[8];
 };
 
+// ------------------------------------------------------------ tile pass
+//
+// A CTA owns a tile of 2^kTileQubits amplitudes: the 5 lowest qubits (the
+// lanes: every warp access is 512 contiguous bytes) plus kTileHigh arbitrary
+// higher qubits. The ops of a pass run in phases; in each phase every thread
+// holds 2^kPhaseRegBits amplitudes in registers spanning 4 of the tile's high
+// qubits (the phase's register qubits), the 8 warps span the other 3. Gates
+// on lane qubits use warp shuffles, gates on register qubits stay in
+// registers, diagonal ops and channels act elementwise anywhere; between
+// phases the tile is re-laid out through shared memory. Phase 0 loads from
+// HBM and the last phase stores to HBM, so a pass is one read + one write of
+// the state whatever its op count.
+constexpr int kTileQubits = 12;
+constexpr int kTileHigh = kTileQubits - kLaneQubits; // 7
+constexpr int kPhaseRegBits = 4;
+constexpr int kTileWarpBits = kTileHigh - kPhaseRegBits; // 3
+constexpr int kTileThreads = 32 << kTileWarpBits;        // 256
+constexpr int kMaxPhases = 8;
+constexpr int kMaxTileOps = 64;
+
+enum TileLoc : uint8_t { TL_LANE = 0, TL_REG = 1, TL_WARP = 2, TL_OUTER = 3 };
+
+struct TileOp {
+    uint8_t kind;    // PassOpKind (PO_PAIR_REG / PO_PAIR_LANE / PO_DIAG / ...)
+    uint8_t cls;     // GateClass
+    uint8_t flags;   // DiagFlags / collapse two-qubit flag
+    uint8_t outcome;
+    uint8_t q0k, q0p, q1k, q1p; // TileLoc kind + position of the op's qubits
+    uint8_t lane_cmask;   // controls on lane bits
+    uint8_t reg_cmask;    // controls on register-index bits
+    uint8_t warp_cmask;   // controls on warp-index bits
+    uint8_t pad[5];
+    uint64_t outer_cmask; // controls on qubits outside the tile (global bits)
+    double m[8];
+};
+static_assert(sizeof(TileOp) == 88, "TileOp layout");
+
+struct TilePhase {
+    uint16_t reg_off[1 << kPhaseRegBits];  // tile index of register i (lane 0, warp 0)
+    uint16_t warp_off[1 << kTileWarpBits]; // tile index offset of warp w
+    uint16_t op_begin, op_end;
+};
+
+struct TileParams {
+    uint64_t num_tiles;
+    uint64_t global_offset;
+    int32_t num_phases;
+    int32_t high_pos[kTileHigh];           // ascending global qubits of tile bits 5..
+    uint64_t seg_off[1 << kTileHigh];      // global offset of tile segment s
+    TilePhase phases[kMaxPhases];
+    TileOp ops[kMaxTileOps];
+};
+
 } // namespace qgpu

@@ -22,6 +22,10 @@ uint64_t launch_count();
 // read + write (kernels.cu: k_fused_pass).
 void launch_pass(double2* amps, const PassParams& params, cudaStream_t s);
 
+// Tile pass (kernels.cu: k_tile_pass): 2^12-amplitude CTA tiles, register
+// phases exchanged through shared memory; one HBM read + write per pass.
+void launch_tile_pass(double2* amps, const TileParams& params, cudaStream_t s);
+
 // One 2x2 gate over all pairs (i, i + 2^t) whose base holds cmask
 // (reference kernels.cpp:43-59). Used for states too small to tile and for
 // the unfused (one pass per gate) mode.

@@ -192,11 +192,43 @@ void QuregImpl::ensure_recv(uint64_t len) {
 }
 
 int QuregImpl::pass_H() const {
-    const int h = std::min(env->reg_qubits, local_qubits - kLaneQubits);
+    const int h = std::min(std::min(env->reg_qubits, 3), local_qubits - kLaneQubits);
     return h < 1 ? 0 : h;
 }
 
+bool QuregImpl::use_tile() const { return local_qubits >= kTileQubits; }
+
 // -------------------------------------------------------------- scheduling
+//
+// Ops are queued in order and cut into passes; no op is ever reordered, so
+// every amplitude sees exactly the reference's sequence of operations.
+// Tile mode (>= 12 local qubits): a pass may touch the 5 lane qubits plus
+// kTileHigh other qubits; inside it, a phase may pair on the lanes plus
+// kPhaseRegBits register qubits. Diagonal gates, dephasing and collapse act
+// elementwise and fit anywhere.
+
+bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
+    if (phases.empty()) phases.push_back(PhaseState{});
+    if (pair && op.q0 >= kLaneQubits) {
+        const int q = op.q0;
+        const bool in_tile = std::find(tile_high.begin(), tile_high.end(), q) != tile_high.end();
+        if (!in_tile && static_cast<int>(tile_high.size()) >= kTileHigh) return false;
+        PhaseState& ph = phases.back();
+        const bool in_phase = std::find(ph.regs.begin(), ph.regs.end(), q) != ph.regs.end();
+        if (!in_phase && static_cast<int>(ph.regs.size()) >= kPhaseRegBits) {
+            if (static_cast<int>(phases.size()) >= kMaxPhases) return false;
+            PhaseState next;
+            next.op_begin = static_cast<int>(pending.size());
+            next.regs.push_back(q);
+            phases.push_back(next);
+        } else if (!in_phase) {
+            ph.regs.push_back(q);
+        }
+        if (!in_tile) tile_high.push_back(q);
+    }
+    pending.push_back(op);
+    return true;
+}
 
 void QuregImpl::enqueue(const FlatOp& op) {
     const bool pair = op.kind == FK_GATE && op.cls != CLS_DIAG;
@@ -216,6 +248,16 @@ void QuregImpl::enqueue(const FlatOp& op) {
         ++passes;
         return;
     }
+    if (use_tile()) {
+        if (!place_tile(op, pair)) {
+            flush();
+            place_tile(op, pair);
+        }
+        if (env->fusion_mode == 1 ||
+            static_cast<int>(pending.size()) >= std::min(env->max_ops, kMaxTileOps))
+            flush();
+        return;
+    }
     if (pair && op.q0 >= kLaneQubits &&
         std::find(regs.begin(), regs.end(), op.q0) == regs.end()) {
         if (static_cast<int>(regs.size()) >= pass_H()) flush();
@@ -226,13 +268,129 @@ void QuregImpl::enqueue(const FlatOp& op) {
 }
 
 void QuregImpl::flush() {
-    if (pending.empty()) {
-        regs.clear();
-        return;
+    if (!pending.empty()) {
+        if (use_tile() && env->fusion_mode != 2)
+            launch_tile();
+        else
+            launch_fused();
     }
-    launch_fused();
-    pending.clear();
-    regs.clear();
+    discard();
+}
+
+void QuregImpl::launch_tile() {
+    // The tile's high qubits: the pass's pair targets, topped up with the
+    // highest unused local qubits (their order only affects the layout).
+    std::vector<int> high = tile_high;
+    for (int q = local_qubits - 1; static_cast<int>(high.size()) < kTileHigh && q >= kLaneQubits; --q)
+        if (std::find(high.begin(), high.end(), q) == high.end()) high.push_back(q);
+    std::sort(high.begin(), high.end());
+    auto tbit = [&](int q) -> int { // tile bit of a local qubit, -1 if outside
+        if (q >= 0 && q < kLaneQubits) return q;
+        for (int j = 0; j < kTileHigh; ++j)
+            if (high[j] == q) return kLaneQubits + j;
+        return -1;
+    };
+
+    TileParams P;
+    std::memset(&P, 0, sizeof(P));
+    P.num_tiles = uint64_t{1} << (local_qubits - kTileQubits);
+    P.num_phases = static_cast<int>(phases.size());
+    for (int j = 0; j < kTileHigh; ++j) P.high_pos[j] = high[j];
+    for (int s = 0; s < (1 << kTileHigh); ++s) {
+        uint64_t off = 0;
+        for (int j = 0; j < kTileHigh; ++j)
+            if ((s >> j) & 1) off |= uint64_t{1} << high[j];
+        P.seg_off[s] = off;
+    }
+    for (size_t p = 0; p < phases.size(); ++p) {
+        TilePhase& Q = P.phases[p];
+        // register bits: the phase's targets, then other tile bits
+        std::vector<int> rb, wb;
+        for (int q : phases[p].regs) rb.push_back(tbit(q));
+        for (int t = kLaneQubits; t < kTileQubits && static_cast<int>(rb.size()) < kPhaseRegBits; ++t)
+            if (std::find(rb.begin(), rb.end(), t) == rb.end()) rb.push_back(t);
+        for (int t = kLaneQubits; t < kTileQubits; ++t)
+            if (std::find(rb.begin(), rb.end(), t) == rb.end()) wb.push_back(t);
+        for (int i = 0; i < (1 << kPhaseRegBits); ++i) {
+            uint32_t off = 0;
+            for (int j = 0; j < kPhaseRegBits; ++j)
+                if ((i >> j) & 1) off |= 1u << rb[j];
+            Q.reg_off[i] = static_cast<uint16_t>(off);
+        }
+        for (int w = 0; w < (1 << kTileWarpBits); ++w) {
+            uint32_t off = 0;
+            for (int j = 0; j < kTileWarpBits; ++j)
+                if ((w >> j) & 1) off |= 1u << wb[j];
+            Q.warp_off[w] = static_cast<uint16_t>(off);
+        }
+        const int begin = phases[p].op_begin;
+        const int end = p + 1 < phases.size() ? phases[p + 1].op_begin : static_cast<int>(pending.size());
+        Q.op_begin = static_cast<uint16_t>(begin);
+        Q.op_end = static_cast<uint16_t>(end);
+        auto loc = [&](int q, uint8_t* kind, uint8_t* pos) {
+            const int t = tbit(q);
+            if (q < 0) {
+                *kind = TL_OUTER;
+                *pos = 0;
+            } else if (t < 0) {
+                *kind = TL_OUTER;
+                *pos = static_cast<uint8_t>(q);
+            } else if (t < kLaneQubits) {
+                *kind = TL_LANE;
+                *pos = static_cast<uint8_t>(t);
+            } else {
+                for (int j = 0; j < kPhaseRegBits; ++j)
+                    if (rb[j] == t) {
+                        *kind = TL_REG;
+                        *pos = static_cast<uint8_t>(j);
+                        return;
+                    }
+                for (int j = 0; j < kTileWarpBits; ++j)
+                    if (wb[j] == t) {
+                        *kind = TL_WARP;
+                        *pos = static_cast<uint8_t>(j);
+                        return;
+                    }
+            }
+        };
+        for (int k = begin; k < end; ++k) {
+            const FlatOp& op = pending[k];
+            TileOp& to = P.ops[k];
+            switch (op.kind) {
+            case FK_GATE:
+                to.kind = op.cls == CLS_DIAG ? PO_DIAG
+                                             : (op.q0 < kLaneQubits ? PO_PAIR_LANE : PO_PAIR_REG);
+                break;
+            case FK_DEPHASE: to.kind = PO_DEPHASE; break;
+            default: to.kind = PO_COLLAPSE; break;
+            }
+            to.cls = op.cls;
+            to.flags = op.kind == FK_COLLAPSE ? (op.q1 >= 0 ? 1 : 0) : op.flags;
+            to.outcome = op.outcome;
+            loc(op.q0, &to.q0k, &to.q0p);
+            loc(op.q1, &to.q1k, &to.q1p);
+            uint64_t outer = op.cmask;
+            for (int q = 0; q < local_qubits; ++q) {
+                if (!((op.cmask >> q) & 1)) continue;
+                uint8_t kind = 0, pos = 0;
+                loc(q, &kind, &pos);
+                if (kind == TL_OUTER) continue;
+                outer &= ~(uint64_t{1} << q);
+                if (kind == TL_LANE) to.lane_cmask |= static_cast<uint8_t>(1u << pos);
+                if (kind == TL_REG) to.reg_cmask |= static_cast<uint8_t>(1u << pos);
+                if (kind == TL_WARP) to.warp_cmask |= static_cast<uint8_t>(1u << pos);
+            }
+            to.outer_cmask = outer;
+            std::memcpy(to.m, op.m, sizeof(to.m));
+        }
+    }
+    ProfScope prof(env, PK_PASS);
+    for (auto& s : shards) {
+        P.global_offset = goff(s);
+        launch_tile_pass(s.amps, P, env->stream);
+    }
+    cuda_check(cudaGetLastError(), "tile pass launch");
+    ++passes;
 }
 
 void QuregImpl::launch_fused() {

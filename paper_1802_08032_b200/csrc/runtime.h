@@ -117,13 +117,24 @@ struct QuregImpl {
 
     // the open pass
     std::vector<FlatOp> pending;
-    std::vector<int> regs;
+    std::vector<int> regs; // register qubits (small-state register pass)
+    struct PhaseState {
+        std::vector<int> regs;
+        int op_begin = 0;
+    };
+    std::vector<int> tile_high;      // tile pass: high qubits in the tile
+    std::vector<PhaseState> phases;  // tile pass: phases
 
     ~QuregImpl();
 
     void enqueue(const FlatOp& op);
     void flush();
-    void discard() { pending.clear(); regs.clear(); }
+    void discard() {
+        pending.clear();
+        regs.clear();
+        tile_high.clear();
+        phases.clear();
+    }
 
     // reductions (flush first; synchronous)
     double reduce_norm(int t, int outcome); // sum |a|^2 (t < 0: all)
@@ -136,6 +147,9 @@ struct QuregImpl {
 
   private:
     int pass_H() const;
+    bool use_tile() const;
+    bool place_tile(const FlatOp& op, bool pair);
+    void launch_tile();
     void run_simple(const FlatOp& op);
     void launch_fused();
     void run_exchange_gate(const FlatOp& op);
