@@ -26,11 +26,11 @@ COMMON = [
     "-Xcompiler", "-fPIC,-O3,-ffp-contract=off",
     f"-I{INCLUDE}", f"-I{CSRC}",
 ]
-SOURCES = ["kernels.cu", "runtime.cpp", "api.cpp", "transport.cpp"]
+SOURCES = ["kernels.cu", "tile_pass.cu", "runtime.cpp", "api.cpp", "transport.cpp"]
 
 
 def _headers() -> list[Path]:
-    return list(CSRC.glob("*.h")) + list(INCLUDE.glob("*.h"))
+    return list(CSRC.glob("*.h")) + list(CSRC.glob("*.cuh")) + list(INCLUDE.glob("*.h"))
 
 
 def _stale(target: Path, deps: list[Path]) -> bool:

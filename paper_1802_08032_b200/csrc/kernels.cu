@@ -1,17 +1,10 @@
-// kernels.cu — hand-written sm_100a kernels for the state-vector /
-// density-matrix gate path. FP64, HBM-bandwidth bound: no tensor cores.
-//
-// Arithmetic parity: every pair update evaluates exactly the fma chain the
-// reference's pair_lo_out / pair_hi_out compile to
-// (/root/reference/proj/include/qsim/detail/pair_math.hpp:30-45, contracted by
-// GCC as read from the reference objects; restated in oracle/qsim_oracle.c):
-//   re = fma(-q3, y1, fma(q2, x1, fma(q0, x0, -(q1 * y0))))
-//   im = fma( q3, x1, fma(q2, y1, fma(q0, y0,   q1 * x0)))
-// with (q0..q3) = (a_re, a_im, b_re, b_im) for the low output and
-// (c_re, c_im, d_re, d_im) for the high one, (x0,y0) = lo, (x1,y1) = hi.
-// Terms with an exactly-zero coefficient are dropped at compile time per gate
-// class (value-identical: such an fma only adds a signed zero). The result is
-// bit-identical to the reference on every amplitude (tests/test_gpu_parity.py).
+// kernels.cu — the sm_100a kernels around the hot tile pass (tile_pass.cu):
+// register-only passes for small states, one-gate-per-launch kernels (the
+// unfused mode), channels, exchange combines, compensated reductions.
+// FP64, HBM-bandwidth bound: no tensor cores. The pair arithmetic is the
+// reference's own fma chain (pair_math.cuh), so results are bit-identical to
+// the reference on every amplitude (tests/test_gpu_parity.py).
+#include "pair_math.cuh"
 #include "qgpu_kernels.h"
 
 #include <atomic>
@@ -22,82 +15,6 @@ namespace qgpu {
 namespace {
 
 std::atomic<uint64_t> g_launches{0};
-
-inline void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
-
-__device__ __forceinline__ uint64_t insert_zero_bit(uint64_t x, int pos) {
-    const uint64_t low = x & ((uint64_t{1} << pos) - 1);
-    return ((x >> pos) << (pos + 1)) | low;
-}
-
-// pair_math.hpp:56-61
-__device__ __forceinline__ uint64_t pair_base_index(uint64_t i, int t) {
-    const uint64_t low_mask = (uint64_t{1} << t) - 1;
-    return ((i & ~low_mask) << 1) | (i & low_mask);
-}
-
-// One output row of the pair update; Z = coefficients known to be zero
-// (bit0 q0, bit1 q1, bit2 q2, bit3 q3).
-template <int Z>
-__device__ __forceinline__ double2 row(double q0, double q1, double q2, double q3,
-                                       double2 lo, double2 hi) {
-    constexpr bool n0 = !(Z & 1), n1 = !(Z & 2), n2 = !(Z & 4), n3 = !(Z & 8);
-    double re, im;
-    if constexpr (n0 && n1) {
-        re = fma(q0, lo.x, -(q1 * lo.y));
-        im = fma(q0, lo.y, q1 * lo.x);
-    } else if constexpr (n0) {
-        re = q0 * lo.x;
-        im = q0 * lo.y;
-    } else if constexpr (n1) {
-        re = -(q1 * lo.y);
-        im = q1 * lo.x;
-    } else {
-        re = 0.0;
-        im = 0.0;
-    }
-    if constexpr (n2) {
-        re = fma(q2, hi.x, re);
-        im = fma(q2, hi.y, im);
-    }
-    if constexpr (n3) {
-        re = fma(-q3, hi.y, re);
-        im = fma(q3, hi.x, im);
-    }
-    return make_double2(re, im);
-}
-
-// Zero patterns of the two rows per class (see GateClass in qgpu_device.h).
-template <int CLS> struct ClassZ;
-template <> struct ClassZ<CLS_GENERIC> { static constexpr int z0 = 0, z1 = 0; };
-template <> struct ClassZ<CLS_REAL> { static constexpr int z0 = 0b1010, z1 = 0b1010; };
-template <> struct ClassZ<CLS_RX> { static constexpr int z0 = 0b0110, z1 = 0b1001; };
-
-template <int CLS>
-__device__ __forceinline__ void pair_update(double2& lo, double2& hi, const double* m) {
-    if constexpr (CLS == CLS_SWAP) {
-        const double2 t = lo;
-        lo = hi;
-        hi = t;
-    } else {
-        const double2 l = lo, h = hi;
-        lo = row<ClassZ<CLS>::z0>(m[0], m[1], m[2], m[3], l, h);
-        hi = row<ClassZ<CLS>::z1>(m[4], m[5], m[6], m[7], l, h);
-    }
-}
-
-// Diagonal gate on one amplitude whose target bit is b: a * v (b = 0) or
-// d * v (b = 1), each with the rounding of its reference row (the a term is
-// the fused first product of the low row; the d term is the second product of
-// the high row, so it rounds the other way round).
-__device__ __forceinline__ double2 diag_mul(const double* m, uint32_t b, double2 v) {
-    const double ar = m[0], ai = m[1], dr = m[6], di = m[7];
-    const double s1 = b ? -di : ar, t1 = b ? v.y : v.x;
-    const double s2 = b ? dr : -ai, t2 = b ? v.x : v.y;
-    const double u1 = b ? di : ar, w1 = b ? v.x : v.y;
-    const double u2 = b ? dr : ai, w2 = b ? v.y : v.x;
-    return make_double2(fma(s1, t1, s2 * t2), fma(u1, w1, u2 * w2));
-}
 
 // ------------------------------------------------------------ fused pass
 
@@ -235,193 +152,6 @@ k_fused_pass(double2* __restrict__ amps, const __grid_constant__ PassParams P) {
         }
 #pragma unroll
         for (int i = 0; i < R; ++i) __stcs(amps + b + P.reg_off[i] + lane, v[i]);
-    }
-}
-
-// ---------------------------------------------------------------- tile pass
-//
-// One CTA per 2^12-amplitude tile (qgpu_device.h: TileParams). The op loop
-// is warp-uniform: every branch below depends only on the op (or on a
-// compile-time register index), never on the lane, except the final selects
-// that apply lane/warp/outer controls.
-
-template <int RB>
-using Regs = double2[1 << RB];
-
-template <int RB, int J, int CLS>
-__device__ __forceinline__ void tile_reg_pair(Regs<RB>& v, const double* c, uint32_t rcm, bool tok) {
-#pragma unroll
-    for (int i = 0; i < (1 << RB); ++i) {
-        if (i & (1 << J)) continue;
-        if ((static_cast<uint32_t>(i) & rcm) != rcm) continue; // uniform
-        double2 lo = v[i], hi = v[i | (1 << J)];
-        pair_update<CLS>(lo, hi, c);
-        if (tok) {
-            v[i] = lo;
-            v[i | (1 << J)] = hi;
-        }
-    }
-}
-
-template <int RB, int CLS>
-__device__ __forceinline__ void tile_reg_dispatch(Regs<RB>& v, const double* c, int J, uint32_t rcm,
-                                                  bool tok) {
-    switch (J) {
-    case 0: tile_reg_pair<RB, 0, CLS>(v, c, rcm, tok); break;
-    case 1: if constexpr (RB > 1) tile_reg_pair<RB, 1, CLS>(v, c, rcm, tok); break;
-    case 2: if constexpr (RB > 2) tile_reg_pair<RB, 2, CLS>(v, c, rcm, tok); break;
-    default: if constexpr (RB > 3) tile_reg_pair<RB, 3, CLS>(v, c, rcm, tok); break;
-    }
-}
-
-template <int RB, int CLS>
-__device__ __forceinline__ void tile_lane_pair(Regs<RB>& v, const double* c, uint32_t b, uint32_t rcm,
-                                               bool tok, uint32_t lane) {
-    const uint32_t mask = 1u << b;
-    const bool own_lo = (lane & mask) == 0;
-    // distributed.cpp:183-184: own_lo ? lo_out(mine, theirs) : hi_out(theirs, mine)
-    const double q0 = own_lo ? c[0] : c[4], q1 = own_lo ? c[1] : c[5];
-    const double q2 = own_lo ? c[2] : c[6], q3 = own_lo ? c[3] : c[7];
-#pragma unroll
-    for (int i = 0; i < (1 << RB); ++i) {
-        if ((static_cast<uint32_t>(i) & rcm) != rcm) continue; // uniform: shuffles stay converged
-        double2 th;
-        th.x = __shfl_xor_sync(0xffffffffu, v[i].x, mask);
-        th.y = __shfl_xor_sync(0xffffffffu, v[i].y, mask);
-        double2 r;
-        if constexpr (CLS == CLS_SWAP) {
-            r = th;
-        } else {
-            const double2 lo = own_lo ? v[i] : th;
-            const double2 hi = own_lo ? th : v[i];
-            r = row<CLS == CLS_REAL ? 0b1010 : 0>(q0, q1, q2, q3, lo, hi);
-        }
-        if (tok) v[i] = r;
-    }
-}
-
-struct BitSrc {
-    bool reg;
-    uint32_t pos, fixed;
-};
-
-__device__ __forceinline__ BitSrc bit_src(uint8_t kind, uint8_t pos, uint32_t lane, uint32_t w,
-                                          uint64_t gbase) {
-    BitSrc s;
-    s.reg = kind == TL_REG;
-    s.pos = pos;
-    s.fixed = kind == TL_LANE   ? (lane >> pos) & 1u
-              : kind == TL_WARP ? (w >> pos) & 1u
-                                : static_cast<uint32_t>((gbase >> pos) & 1u);
-    return s;
-}
-
-__device__ __forceinline__ uint32_t bit_at(const BitSrc& s, int i) {
-    return s.reg ? (static_cast<uint32_t>(i) >> s.pos) & 1u : s.fixed;
-}
-
-template <int RB>
-__device__ __forceinline__ void tile_apply(Regs<RB>& v, const TileOp& op, uint32_t lane, uint32_t w,
-                                           uint64_t gbase) {
-    const bool tok = (lane & op.lane_cmask) == op.lane_cmask &&
-                     (w & op.warp_cmask) == op.warp_cmask &&
-                     (gbase & op.outer_cmask) == op.outer_cmask;
-    const uint32_t rcm = op.reg_cmask;
-    double c[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) c[k] = op.m[k];
-    switch (op.kind) {
-    case PO_PAIR_REG:
-        switch (op.cls) {
-        case CLS_SWAP: tile_reg_dispatch<RB, CLS_SWAP>(v, c, op.q0p, rcm, tok); break;
-        case CLS_REAL: tile_reg_dispatch<RB, CLS_REAL>(v, c, op.q0p, rcm, tok); break;
-        case CLS_RX: tile_reg_dispatch<RB, CLS_RX>(v, c, op.q0p, rcm, tok); break;
-        default: tile_reg_dispatch<RB, CLS_GENERIC>(v, c, op.q0p, rcm, tok); break;
-        }
-        break;
-    case PO_PAIR_LANE:
-        switch (op.cls) {
-        case CLS_SWAP: tile_lane_pair<RB, CLS_SWAP>(v, c, op.q0p, rcm, tok, lane); break;
-        case CLS_REAL: tile_lane_pair<RB, CLS_REAL>(v, c, op.q0p, rcm, tok, lane); break;
-        default: tile_lane_pair<RB, CLS_GENERIC>(v, c, op.q0p, rcm, tok, lane); break;
-        }
-        break;
-    case PO_DIAG: {
-        const BitSrc s0 = bit_src(op.q0k, op.q0p, lane, w, gbase);
-        const bool a_one = op.flags & DF_A_ONE, d_one = op.flags & DF_D_ONE;
-#pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            if ((static_cast<uint32_t>(i) & rcm) != rcm) continue;
-            const uint32_t b = bit_at(s0, i);
-            const double2 r = diag_mul(c, b, v[i]);
-            if (tok && !(b ? d_one : a_one)) v[i] = r;
-        }
-        break;
-    }
-    case PO_DEPHASE: { // density.cpp:56-59
-        const BitSrc s0 = bit_src(op.q0k, op.q0p, lane, w, gbase);
-        const BitSrc s1 = bit_src(op.q1k, op.q1p, lane, w, gbase);
-#pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            if (bit_at(s0, i) != bit_at(s1, i)) {
-                v[i].x *= c[0];
-                v[i].y *= c[0];
-            }
-        }
-        break;
-    }
-    default: { // PO_COLLAPSE
-        const BitSrc s0 = bit_src(op.q0k, op.q0p, lane, w, gbase);
-        const BitSrc s1 = bit_src(op.q1k, op.q1p, lane, w, gbase);
-        const uint32_t o = op.outcome;
-        const bool two = op.flags & 1;
-#pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            const bool keep = bit_at(s0, i) == o && (!two || bit_at(s1, i) == o);
-            v[i].x = keep ? v[i].x * c[0] : 0.0;
-            v[i].y = keep ? v[i].y * c[0] : 0.0;
-        }
-        break;
-    }
-    }
-}
-
-template <int RB, int WB>
-__global__ void __launch_bounds__(32 << WB, 2)
-k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
-    constexpr int R = 1 << RB;
-    extern __shared__ double2 tile[];
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t w = threadIdx.x >> 5;
-    const int nph = P.num_phases;
-    for (uint64_t T = blockIdx.x; T < P.num_tiles; T += gridDim.x) {
-        uint64_t gb = T << kLaneQubits;
-#pragma unroll
-        for (int j = 0; j < RB + WB; ++j) gb = insert_zero_bit(gb, P.high_pos[j]);
-        const uint64_t gbase = gb + P.global_offset;
-        double2* base = amps + gb + lane;
-        double2 v[R];
-        for (int ph = 0; ph < nph; ++ph) {
-            const TilePhase& Q = P.phases[ph];
-            const uint32_t wofs = Q.warp_off[w];
-            if (ph == 0) {
-#pragma unroll
-                for (int i = 0; i < R; ++i) v[i] = __ldcs(base + P.seg_off[(wofs + Q.reg_off[i]) >> 5]);
-            } else {
-                __syncthreads();
-#pragma unroll
-                for (int i = 0; i < R; ++i) v[i] = tile[wofs + Q.reg_off[i] + lane];
-            }
-            for (int o = Q.op_begin; o < Q.op_end; ++o) tile_apply<RB>(v, P.ops[o], lane, w, gbase);
-            if (ph == nph - 1) {
-#pragma unroll
-                for (int i = 0; i < R; ++i) __stcs(base + P.seg_off[(wofs + Q.reg_off[i]) >> 5], v[i]);
-            } else {
-#pragma unroll
-                for (int i = 0; i < R; ++i) tile[wofs + Q.reg_off[i] + lane] = v[i];
-            }
-        }
-        if (nph > 1) __syncthreads();
     }
 }
 
@@ -646,6 +376,8 @@ __global__ void k_fill(double2* __restrict__ amps, uint64_t len, double2 value) 
 
 uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
 void launch_pass(double2* amps, const PassParams& p, cudaStream_t s) {
     constexpr int threads = 256;
     const uint64_t warps = p.num_tiles;
@@ -658,23 +390,6 @@ void launch_pass(double2* amps, const PassParams& p, cudaStream_t s) {
     case 2: k_fused_pass<2><<<static_cast<unsigned>(blocks), threads, 0, s>>>(amps, p); break;
     default: k_fused_pass<3><<<static_cast<unsigned>(blocks), threads, 0, s>>>(amps, p); break;
     }
-    count_launch();
-}
-
-void launch_tile_pass(double2* amps, const TileParams& p, cudaStream_t s) {
-    auto kern = k_tile_pass<kPhaseRegBits, kTileWarpBits>;
-    constexpr size_t smem_tile = sizeof(double2) << kTileQubits;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem_tile));
-        attr_set = true;
-    }
-    uint64_t blocks = p.num_tiles;
-    const uint64_t cap = 148ull * 2ull; // persistent: 2 CTAs per SM
-    if (blocks > cap) blocks = cap;
-    const size_t smem = p.num_phases > 1 ? smem_tile : 0;
-    kern<<<static_cast<unsigned>(blocks), kTileThreads, smem, s>>>(amps, p);
     count_launch();
 }
 

@@ -91,7 +91,10 @@ struct Mat2 {
 // the state whatever its op count.
 constexpr int kTileQubits = 12;
 constexpr int kTileHigh = kTileQubits - kLaneQubits; // 7
-constexpr int kPhaseRegBits = 4;
+#ifndef QGPU_PHASE_REG_BITS
+#define QGPU_PHASE_REG_BITS 4
+#endif
+constexpr int kPhaseRegBits = QGPU_PHASE_REG_BITS;
 constexpr int kTileWarpBits = kTileHigh - kPhaseRegBits; // 3
 constexpr int kTileThreads = 32 << kTileWarpBits;        // 256
 constexpr int kMaxPhases = 8;
@@ -99,31 +102,56 @@ constexpr int kMaxTileOps = 64;
 
 enum TileLoc : uint8_t { TL_LANE = 0, TL_REG = 1, TL_WARP = 2, TL_OUTER = 3 };
 
+// Handler codes of the tile pass, resolved on the host so the kernel
+// dispatches each op with one jump table (tile_pass.cu: step).
+enum TileCode : uint8_t {
+    TC_REG = 0,      // + 4 * {GENERIC, REAL, RX, SWAP} + register bit: 0..15
+    TC_REG_SEL = 16, // + 4 * {GENERIC, SWAP} + register bit (controlled): 16..23
+    TC_LANE_GENERIC = 24,
+    TC_LANE_REAL = 25,
+    TC_LANE_SWAP = 26,
+    TC_LANE_SEL_GENERIC = 27,
+    TC_LANE_SEL_SWAP = 28,
+    TC_DIAG_REG = 29, // + register bit: 29..32
+    TC_DIAG_FIXED = 33,
+    TC_DEPHASE = 34,
+    TC_COLLAPSE = 35,
+};
+
+// Op header packed in one 64-bit word (one constant-bank load per op):
+//   [0,6) TileCode  [6,10) flags  [10] outcome  [11,13) q0 TileLoc
+//   [13,19) q0 pos  [19,21) q1 TileLoc  [21,27) q1 pos  [27,32) lane cmask
+//   [32,36) register cmask  [36,40) warp cmask
 struct TileOp {
-    uint8_t kind;    // PassOpKind (PO_PAIR_REG / PO_PAIR_LANE / PO_DIAG / ...)
-    uint8_t cls;     // GateClass
-    uint8_t flags;   // DiagFlags / collapse two-qubit flag
-    uint8_t outcome;
-    uint8_t q0k, q0p, q1k, q1p; // TileLoc kind + position of the op's qubits
-    uint8_t lane_cmask;   // controls on lane bits
-    uint8_t reg_cmask;    // controls on register-index bits
-    uint8_t warp_cmask;   // controls on warp-index bits
-    uint8_t pad[5];
+    uint64_t hdr;
     uint64_t outer_cmask; // controls on qubits outside the tile (global bits)
     double m[8];
 };
-static_assert(sizeof(TileOp) == 88, "TileOp layout");
+static_assert(sizeof(TileOp) == 80, "TileOp layout");
+
+constexpr uint64_t tile_hdr(uint32_t code, uint32_t flags, uint32_t outcome,
+                            uint32_t q0k, uint32_t q0p, uint32_t q1k, uint32_t q1p,
+                            uint32_t lane_cm, uint32_t reg_cm, uint32_t warp_cm) {
+    return uint64_t(code & 63) | uint64_t(flags & 15) << 6 |
+           uint64_t(outcome & 1) << 10 | uint64_t(q0k & 3) << 11 | uint64_t(q0p & 63) << 13 |
+           uint64_t(q1k & 3) << 19 | uint64_t(q1p & 63) << 21 | uint64_t(lane_cm & 31) << 27 |
+           uint64_t(reg_cm & 15) << 32 | uint64_t(warp_cm & 15) << 36;
+}
 
 struct TilePhase {
     uint16_t reg_off[1 << kPhaseRegBits];  // tile index of register i (lane 0, warp 0)
     uint16_t warp_off[1 << kTileWarpBits]; // tile index offset of warp w
     uint16_t op_begin, op_end;
+    // index of the (single) register-pair op on register bit j, 0xFFFF if
+    // none; increasing in j (kernels.cu: run_phase_ops)
+    uint16_t reg_at[kPhaseRegBits];
 };
 
 struct TileParams {
     uint64_t num_tiles;
     uint64_t global_offset;
     int32_t num_phases;
+    int32_t seg_run;                       // high_pos[0..seg_run) = 5, 6, ...: contiguous
     int32_t high_pos[kTileHigh];           // ascending global qubits of tile bits 5..
     uint64_t seg_off[1 << kTileHigh];      // global offset of tile segment s
     TilePhase phases[kMaxPhases];

@@ -17,13 +17,15 @@ constexpr int kReduceThreads = 256;
 // Kernel launches issued by this library since load (the bench's
 // gpu_launches and the tests' evidence that the CUDA path ran).
 uint64_t launch_count();
+void count_launch(); // internal: every launcher calls it once per kernel
 
 // Fused pass: applies params.ops in order to every amplitude in one HBM
 // read + write (kernels.cu: k_fused_pass).
 void launch_pass(double2* amps, const PassParams& params, cudaStream_t s);
 
-// Tile pass (kernels.cu: k_tile_pass): 2^12-amplitude CTA tiles, register
-// phases exchanged through shared memory; one HBM read + write per pass.
+// Tile pass (tile_pass.cu: k_tile_pass): 2^12-amplitude tiles streamed through
+// shared memory by TMA, ops applied in register phases; one HBM read + write
+// per pass.
 void launch_tile_pass(double2* amps, const TileParams& params, cudaStream_t s);
 
 // One 2x2 gate over all pairs (i, i + 2^t) whose base holds cmask

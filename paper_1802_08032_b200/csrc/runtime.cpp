@@ -213,17 +213,17 @@ bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
         const int q = op.q0;
         const bool in_tile = std::find(tile_high.begin(), tile_high.end(), q) != tile_high.end();
         if (!in_tile && static_cast<int>(tile_high.size()) >= kTileHigh) return false;
+        // one register op per register bit per phase (kernels.cu: run_phase_ops)
         PhaseState& ph = phases.back();
         const bool in_phase = std::find(ph.regs.begin(), ph.regs.end(), q) != ph.regs.end();
-        if (!in_phase && static_cast<int>(ph.regs.size()) >= kPhaseRegBits) {
+        if (in_phase || static_cast<int>(ph.regs.size()) >= kPhaseRegBits) {
             if (static_cast<int>(phases.size()) >= kMaxPhases) return false;
             PhaseState next;
             next.op_begin = static_cast<int>(pending.size());
-            next.regs.push_back(q);
             phases.push_back(next);
-        } else if (!in_phase) {
-            ph.regs.push_back(q);
         }
+        phases.back().regs.push_back(q);
+        phases.back().reg_ops.push_back(static_cast<int>(pending.size()));
         if (!in_tile) tile_high.push_back(q);
     }
     pending.push_back(op);
@@ -279,11 +279,14 @@ void QuregImpl::flush() {
 
 void QuregImpl::launch_tile() {
     // The tile's high qubits: the pass's pair targets, topped up with the
-    // highest unused local qubits (their order only affects the layout).
+    // lowest unused local qubits, so that qubits 5, 6, ... extend the
+    // contiguous 512 B segments into longer runs (fewer, larger bulk copies).
     std::vector<int> high = tile_high;
-    for (int q = local_qubits - 1; static_cast<int>(high.size()) < kTileHigh && q >= kLaneQubits; --q)
+    for (int q = kLaneQubits; static_cast<int>(high.size()) < kTileHigh && q < local_qubits; ++q)
         if (std::find(high.begin(), high.end(), q) == high.end()) high.push_back(q);
     std::sort(high.begin(), high.end());
+    int seg_run = 0;
+    while (seg_run < kTileHigh && high[seg_run] == kLaneQubits + seg_run) ++seg_run;
     auto tbit = [&](int q) -> int { // tile bit of a local qubit, -1 if outside
         if (q >= 0 && q < kLaneQubits) return q;
         for (int j = 0; j < kTileHigh; ++j)
@@ -295,6 +298,7 @@ void QuregImpl::launch_tile() {
     std::memset(&P, 0, sizeof(P));
     P.num_tiles = uint64_t{1} << (local_qubits - kTileQubits);
     P.num_phases = static_cast<int>(phases.size());
+    P.seg_run = std::min(seg_run, 5); // copies of up to 32 segments (16 KiB)
     for (int j = 0; j < kTileHigh; ++j) P.high_pos[j] = high[j];
     for (int s = 0; s < (1 << kTileHigh); ++s) {
         uint64_t off = 0;
@@ -327,6 +331,10 @@ void QuregImpl::launch_tile() {
         const int end = p + 1 < phases.size() ? phases[p + 1].op_begin : static_cast<int>(pending.size());
         Q.op_begin = static_cast<uint16_t>(begin);
         Q.op_end = static_cast<uint16_t>(end);
+        for (int j = 0; j < kPhaseRegBits; ++j)
+            Q.reg_at[j] = j < static_cast<int>(phases[p].reg_ops.size())
+                              ? static_cast<uint16_t>(phases[p].reg_ops[j])
+                              : uint16_t{0xFFFF};
         auto loc = [&](int q, uint8_t* kind, uint8_t* pos) {
             const int t = tbit(q);
             if (q < 0) {
@@ -356,30 +364,47 @@ void QuregImpl::launch_tile() {
         for (int k = begin; k < end; ++k) {
             const FlatOp& op = pending[k];
             TileOp& to = P.ops[k];
-            switch (op.kind) {
-            case FK_GATE:
-                to.kind = op.cls == CLS_DIAG ? PO_DIAG
-                                             : (op.q0 < kLaneQubits ? PO_PAIR_LANE : PO_PAIR_REG);
-                break;
-            case FK_DEPHASE: to.kind = PO_DEPHASE; break;
-            default: to.kind = PO_COLLAPSE; break;
-            }
-            to.cls = op.cls;
-            to.flags = op.kind == FK_COLLAPSE ? (op.q1 >= 0 ? 1 : 0) : op.flags;
-            to.outcome = op.outcome;
-            loc(op.q0, &to.q0k, &to.q0p);
-            loc(op.q1, &to.q1k, &to.q1p);
+            const uint32_t flags = op.kind == FK_COLLAPSE ? (op.q1 >= 0 ? 1 : 0) : op.flags;
+            uint8_t q0k = 0, q0p = 0, q1k = 0, q1p = 0;
+            loc(op.q0, &q0k, &q0p);
+            loc(op.q1, &q1k, &q1p);
+            uint32_t lane_cm = 0, reg_cm = 0, warp_cm = 0;
             uint64_t outer = op.cmask;
             for (int q = 0; q < local_qubits; ++q) {
                 if (!((op.cmask >> q) & 1)) continue;
-                uint8_t kind = 0, pos = 0;
-                loc(q, &kind, &pos);
-                if (kind == TL_OUTER) continue;
+                uint8_t ck = 0, cp = 0;
+                loc(q, &ck, &cp);
+                if (ck == TL_OUTER) continue;
                 outer &= ~(uint64_t{1} << q);
-                if (kind == TL_LANE) to.lane_cmask |= static_cast<uint8_t>(1u << pos);
-                if (kind == TL_REG) to.reg_cmask |= static_cast<uint8_t>(1u << pos);
-                if (kind == TL_WARP) to.warp_cmask |= static_cast<uint8_t>(1u << pos);
+                if (ck == TL_LANE) lane_cm |= 1u << cp;
+                if (ck == TL_REG) reg_cm |= 1u << cp;
+                if (ck == TL_WARP) warp_cm |= 1u << cp;
             }
+            // resolve the kernel's handler (qgpu_device.h: TileCode)
+            const bool ctrl = op.cmask != 0;
+            uint32_t code;
+            if (op.kind == FK_DEPHASE) {
+                code = TC_DEPHASE;
+            } else if (op.kind == FK_COLLAPSE) {
+                code = TC_COLLAPSE;
+            } else if (op.cls == CLS_DIAG) {
+                code = q0k == TL_REG ? TC_DIAG_REG + q0p : TC_DIAG_FIXED;
+            } else if (q0k == TL_LANE) {
+                if (!ctrl)
+                    code = op.cls == CLS_SWAP   ? TC_LANE_SWAP
+                           : op.cls == CLS_REAL ? TC_LANE_REAL
+                                                : TC_LANE_GENERIC;
+                else
+                    code = op.cls == CLS_SWAP ? TC_LANE_SEL_SWAP : TC_LANE_SEL_GENERIC;
+            } else { // register bit
+                if (!ctrl) {
+                    const uint32_t row = op.cls == CLS_REAL ? 1 : op.cls == CLS_RX ? 2 : op.cls == CLS_SWAP ? 3 : 0;
+                    code = TC_REG + 4 * row + q0p;
+                } else {
+                    code = TC_REG_SEL + 4 * (op.cls == CLS_SWAP ? 1 : 0) + q0p;
+                }
+            }
+            to.hdr = tile_hdr(code, flags, op.outcome, q0k, q0p, q1k, q1p, lane_cm, reg_cm, warp_cm);
             to.outer_cmask = outer;
             std::memcpy(to.m, op.m, sizeof(to.m));
         }

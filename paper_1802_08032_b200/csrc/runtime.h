@@ -119,7 +119,8 @@ struct QuregImpl {
     std::vector<FlatOp> pending;
     std::vector<int> regs; // register qubits (small-state register pass)
     struct PhaseState {
-        std::vector<int> regs;
+        std::vector<int> regs;    // register qubits, in order of their (single) op
+        std::vector<int> reg_ops; // index of that op in `pending`
         int op_begin = 0;
     };
     std::vector<int> tile_high;      // tile pass: high qubits in the tile

@@ -15,7 +15,7 @@ from pathlib import Path
 
 import numpy as np
 
-LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libqgpu.so"
+LIB_PATH = Path(os.environ.get("QGPU_LIB") or Path(__file__).resolve().parent / "_lib" / "libqgpu.so")
 
 
 class QuESTError(RuntimeError):
