@@ -257,6 +257,13 @@ def run_ours(args):
 
     # roofline of the dominant kernel (the fused pass)
     pk, src = peaks()
+    traffic = None
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())["k_tile_pass"]
+        if t["local_qubits"] == args.local_qubits:
+            traffic = t["bytes"]
+    except Exception:
+        pass
     pass_ms = ms_launch[kinds == 0]
     exch_ms = ms_launch[kinds == 2]
     per_launch_bytes = 2.0 * 16.0 * (2.0 ** args.local_qubits)
@@ -314,7 +321,7 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                          "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / pk["hbm_gbs"], 4) if achieved else None,
-                         "traffic": None, "kernel": "k_tile_pass", "peak_source": src,
+                         "traffic": traffic, "kernel": "k_tile_pass", "peak_source": src,
                          "bytes_per_launch": per_launch_bytes,
                          "avg_launch_ms": round(float(pass_ms.mean()), 4) if pass_ms.size else None,
                          "launches": int(pass_ms.size), "share_of_step": round(share, 4) if share else None},

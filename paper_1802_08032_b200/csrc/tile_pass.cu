@@ -133,6 +133,29 @@ __device__ __forceinline__ void h_reg_pair(const Regs<RB>& s, Regs<RB>& d, const
     }
 }
 
+// In-place form of h_reg_pair (one array): pair by pair, both outputs are
+// computed before either input is overwritten.
+template <int RB, int J, int CLS, bool SEL>
+__device__ __forceinline__ void h_reg_pair_ip(Regs<RB>& v, const double* c, uint32_t rcm, bool tok) {
+    if constexpr (J < RB) {
+#pragma unroll
+        for (int lo = 0; lo < (1 << RB); ++lo) {
+            constexpr int bit = 1 << J;
+            if (lo & bit) continue;
+            double2 l = v[lo], h = v[lo | bit];
+            pair_update<CLS>(l, h, c);
+            if constexpr (SEL) {
+                const bool on = tok && (static_cast<uint32_t>(lo) & rcm) == rcm;
+                v[lo] = on ? l : v[lo];
+                v[lo | bit] = on ? h : v[lo | bit];
+            } else {
+                v[lo] = l;
+                v[lo | bit] = h;
+            }
+        }
+    }
+}
+
 // 2x2 gate on lane bit b: the partner amplitude comes from lane ^ 2^b, and
 // each lane computes its own half (distributed.cpp:183-184:
 // own_lo ? lo_out(mine, theirs) : hi_out(theirs, mine)).
@@ -212,10 +235,24 @@ __device__ __forceinline__ uint32_t fixed_bit_of(uint32_t kind, uint32_t pos, ui
 // so its constant-bank latency hides behind the previous op; its low 6 bits
 // are the handler code the host resolved (qgpu_device.h: TileCode), so
 // dispatch is a single jump table.
-template <int RB>
+template <int RB, bool IP, int J, int CLS, bool SEL>
+__device__ __forceinline__ void reg_op(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t rcm,
+                                       bool tok) {
+    if constexpr (J < RB) {
+        if constexpr (IP)
+            h_reg_pair_ip<RB, J, CLS, SEL>(d, c, rcm, tok);
+        else
+            h_reg_pair<RB, J, CLS, SEL>(s, d, c, rcm, tok);
+    }
+}
+
+// IP (in place): s and d are the same array; every handler but the register
+// pairs is elementwise (reads element i before writing it), so only those
+// switch to their pairwise in-place form.
+template <int RB, bool IP>
 __device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, uint64_t h, const TileOp& op,
                                      uint32_t lane, uint32_t w, uint64_t gbase) {
-    static_assert(RB == 4, "register-bit dispatch is written for 4 register qubits");
+    static_assert(RB <= 4, "register-bit dispatch is written for up to 4 register qubits");
     const uint32_t code = h & 63u, flags = (h >> 6) & 15u;
     const uint32_t q0k = (h >> 11) & 3u, q0p = (h >> 13) & 63u;
     const uint32_t lane_cm = (h >> 27) & 31u, rcm = (h >> 32) & 15u, warp_cm = (h >> 36) & 15u;
@@ -227,30 +264,30 @@ __device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, uint64_t h,
     const bool a_one = flags & DF_A_ONE, d_one = flags & DF_D_ONE;
     const double* c = op.m; // coefficients are read from the constant bank where used
     switch (code) {
-    case TC_REG + 0: h_reg_pair<RB, 0, CLS_GENERIC, false>(s, d, c, 0, true); break;
-    case TC_REG + 1: h_reg_pair<RB, 1, CLS_GENERIC, false>(s, d, c, 0, true); break;
-    case TC_REG + 2: h_reg_pair<RB, 2, CLS_GENERIC, false>(s, d, c, 0, true); break;
-    case TC_REG + 3: h_reg_pair<RB, 3, CLS_GENERIC, false>(s, d, c, 0, true); break;
-    case TC_REG + 4: h_reg_pair<RB, 0, CLS_REAL, false>(s, d, c, 0, true); break;
-    case TC_REG + 5: h_reg_pair<RB, 1, CLS_REAL, false>(s, d, c, 0, true); break;
-    case TC_REG + 6: h_reg_pair<RB, 2, CLS_REAL, false>(s, d, c, 0, true); break;
-    case TC_REG + 7: h_reg_pair<RB, 3, CLS_REAL, false>(s, d, c, 0, true); break;
-    case TC_REG + 8: h_reg_pair<RB, 0, CLS_RX, false>(s, d, c, 0, true); break;
-    case TC_REG + 9: h_reg_pair<RB, 1, CLS_RX, false>(s, d, c, 0, true); break;
-    case TC_REG + 10: h_reg_pair<RB, 2, CLS_RX, false>(s, d, c, 0, true); break;
-    case TC_REG + 11: h_reg_pair<RB, 3, CLS_RX, false>(s, d, c, 0, true); break;
-    case TC_REG + 12: h_reg_pair<RB, 0, CLS_SWAP, false>(s, d, c, 0, true); break;
-    case TC_REG + 13: h_reg_pair<RB, 1, CLS_SWAP, false>(s, d, c, 0, true); break;
-    case TC_REG + 14: h_reg_pair<RB, 2, CLS_SWAP, false>(s, d, c, 0, true); break;
-    case TC_REG + 15: h_reg_pair<RB, 3, CLS_SWAP, false>(s, d, c, 0, true); break;
-    case TC_REG_SEL + 0: h_reg_pair<RB, 0, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 1: h_reg_pair<RB, 1, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 2: h_reg_pair<RB, 2, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 3: h_reg_pair<RB, 3, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 4: h_reg_pair<RB, 0, CLS_SWAP, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 5: h_reg_pair<RB, 1, CLS_SWAP, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 6: h_reg_pair<RB, 2, CLS_SWAP, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 7: h_reg_pair<RB, 3, CLS_SWAP, true>(s, d, c, rcm, tok); break;
+    case TC_REG + 0: reg_op<RB, IP,0, CLS_GENERIC, false>(s, d, c, 0, true); break;
+    case TC_REG + 1: reg_op<RB, IP,1, CLS_GENERIC, false>(s, d, c, 0, true); break;
+    case TC_REG + 2: reg_op<RB, IP,2, CLS_GENERIC, false>(s, d, c, 0, true); break;
+    case TC_REG + 3: reg_op<RB, IP,3, CLS_GENERIC, false>(s, d, c, 0, true); break;
+    case TC_REG + 4: reg_op<RB, IP,0, CLS_REAL, false>(s, d, c, 0, true); break;
+    case TC_REG + 5: reg_op<RB, IP,1, CLS_REAL, false>(s, d, c, 0, true); break;
+    case TC_REG + 6: reg_op<RB, IP,2, CLS_REAL, false>(s, d, c, 0, true); break;
+    case TC_REG + 7: reg_op<RB, IP,3, CLS_REAL, false>(s, d, c, 0, true); break;
+    case TC_REG + 8: reg_op<RB, IP,0, CLS_RX, false>(s, d, c, 0, true); break;
+    case TC_REG + 9: reg_op<RB, IP,1, CLS_RX, false>(s, d, c, 0, true); break;
+    case TC_REG + 10: reg_op<RB, IP,2, CLS_RX, false>(s, d, c, 0, true); break;
+    case TC_REG + 11: reg_op<RB, IP,3, CLS_RX, false>(s, d, c, 0, true); break;
+    case TC_REG + 12: reg_op<RB, IP,0, CLS_SWAP, false>(s, d, c, 0, true); break;
+    case TC_REG + 13: reg_op<RB, IP,1, CLS_SWAP, false>(s, d, c, 0, true); break;
+    case TC_REG + 14: reg_op<RB, IP,2, CLS_SWAP, false>(s, d, c, 0, true); break;
+    case TC_REG + 15: reg_op<RB, IP,3, CLS_SWAP, false>(s, d, c, 0, true); break;
+    case TC_REG_SEL + 0: reg_op<RB, IP,0, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
+    case TC_REG_SEL + 1: reg_op<RB, IP,1, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
+    case TC_REG_SEL + 2: reg_op<RB, IP,2, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
+    case TC_REG_SEL + 3: reg_op<RB, IP,3, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
+    case TC_REG_SEL + 4: reg_op<RB, IP,0, CLS_SWAP, true>(s, d, c, rcm, tok); break;
+    case TC_REG_SEL + 5: reg_op<RB, IP,1, CLS_SWAP, true>(s, d, c, rcm, tok); break;
+    case TC_REG_SEL + 6: reg_op<RB, IP,2, CLS_SWAP, true>(s, d, c, rcm, tok); break;
+    case TC_REG_SEL + 7: reg_op<RB, IP,3, CLS_SWAP, true>(s, d, c, rcm, tok); break;
     case TC_LANE_GENERIC: h_lane_pair<RB, CLS_GENERIC, false>(s, d, c, q0p, 0, true, lane); break;
     case TC_LANE_REAL: h_lane_pair<RB, CLS_REAL, false>(s, d, c, q0p, 0, true, lane); break;
     case TC_LANE_SWAP: h_lane_pair<RB, CLS_SWAP, false>(s, d, c, q0p, 0, true, lane); break;
@@ -320,7 +357,7 @@ __device__ __forceinline__ void consumer_sync() {
 // done[b]: the consumers have written stage b's last phase (one arrival per
 // consumer warp); the producer then bulk-stores it and, once the store has
 // read the stage, refills it with the tile NBUF ahead.
-template <int RB, int WB, int NBUF>
+template <int RB, int WB, int NBUF, bool INPLACE>
 __global__ void __launch_bounds__((32 << WB) + 32, 1) // 9 warps: <= 168 registers
 k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
     constexpr int R = 1 << RB;
@@ -391,25 +428,38 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
             if (ph > 0) consumer_sync<32 * NCW>(); // previous phase's writes are in
             const TilePhase& Q = P.phases[ph];
             const uint32_t wofs = Q.warp_off[w] + lane;
-            double2 A[R], B[R];
-#pragma unroll
-            for (int i = 0; i < R; ++i) A[i] = buf[wofs + Q.reg_off[i]];
             const int end = Q.op_end;
             int o = Q.op_begin;
             uint64_t h = o < end ? P.ops[o].hdr : 0; // headers are read one op ahead
-            for (; o + 1 < end; o += 2) {
-                const uint64_t h1 = P.ops[o + 1].hdr;
-                step<RB>(A, B, h, P.ops[o], lane, w, gbase);
-                h = o + 2 < end ? P.ops[o + 2].hdr : 0;
-                step<RB>(B, A, h1, P.ops[o + 1], lane, w, gbase);
-            }
-            if (o < end) {
-                step<RB>(A, B, h, P.ops[o], lane, w, gbase);
+            if constexpr (INPLACE) {
+                double2 A[R];
 #pragma unroll
-                for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = B[i];
-            } else {
+                for (int i = 0; i < R; ++i) A[i] = buf[wofs + Q.reg_off[i]];
+                for (; o < end; ++o) {
+                    const uint64_t hn = o + 1 < end ? P.ops[o + 1].hdr : 0;
+                    step<RB, true>(A, A, h, P.ops[o], lane, w, gbase);
+                    h = hn;
+                }
 #pragma unroll
                 for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = A[i];
+            } else {
+                double2 A[R], B[R];
+#pragma unroll
+                for (int i = 0; i < R; ++i) A[i] = buf[wofs + Q.reg_off[i]];
+                for (; o + 1 < end; o += 2) {
+                    const uint64_t h1 = P.ops[o + 1].hdr;
+                    step<RB, false>(A, B, h, P.ops[o], lane, w, gbase);
+                    h = o + 2 < end ? P.ops[o + 2].hdr : 0;
+                    step<RB, false>(B, A, h1, P.ops[o + 1], lane, w, gbase);
+                }
+                if (o < end) {
+                    step<RB, false>(A, B, h, P.ops[o], lane, w, gbase);
+#pragma unroll
+                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = B[i];
+                } else {
+#pragma unroll
+                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = A[i];
+                }
             }
         }
         fence_proxy_async(); // generic-proxy writes -> visible to the bulk store
@@ -422,7 +472,10 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
 
 void launch_tile_pass(double2* amps, const TileParams& p, cudaStream_t s) {
     constexpr int NBUF = 3;
-    auto kern = k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF>;
+#ifndef QGPU_TILE_INPLACE
+#define QGPU_TILE_INPLACE 0
+#endif
+    auto kern = k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF, QGPU_TILE_INPLACE != 0>;
     constexpr size_t smem = NBUF * (sizeof(double2) << kTileQubits);
     static bool set = false;
     if (!set) {
