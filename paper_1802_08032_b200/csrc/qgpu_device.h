@@ -103,19 +103,27 @@ constexpr int kMaxTileOps = 64;
 enum TileLoc : uint8_t { TL_LANE = 0, TL_REG = 1, TL_WARP = 2, TL_OUTER = 3 };
 
 // Handler codes of the tile pass, resolved on the host so the kernel
-// dispatches each op with one jump table (tile_pass.cu: step).
+// dispatches each op with one jump table (tile_pass.cu: apply). "SEL" codes
+// carry controls on lane or register qubits (a per-element predicate);
+// controls on warp or outer qubits are uniform per warp and skip the op.
 enum TileCode : uint8_t {
     TC_REG = 0,      // + 4 * {GENERIC, REAL, RX, SWAP} + register bit: 0..15
-    TC_REG_SEL = 16, // + 4 * {GENERIC, SWAP} + register bit (controlled): 16..23
+    TC_REG_SEL = 16, // + 4 * {GENERIC, SWAP} + register bit: 16..23
     TC_LANE_GENERIC = 24,
     TC_LANE_REAL = 25,
     TC_LANE_SWAP = 26,
     TC_LANE_SEL_GENERIC = 27,
     TC_LANE_SEL_SWAP = 28,
-    TC_DIAG_REG = 29, // + register bit: 29..32
-    TC_DIAG_FIXED = 33,
-    TC_DEPHASE = 34,
-    TC_COLLAPSE = 35,
+    TC_DIAG_REG = 29,       // + register bit: both sides (Rz, diag(a, d))
+    TC_DIAG_REG_D = 33,     // + register bit: a == 1 (Z, S, T, phase shift)
+    TC_DIAG_REG_SEL = 37,   // + register bit
+    TC_DIAG_REG_D_SEL = 41, // + register bit
+    TC_DIAG_LANE = 45,      // target on a lane qubit
+    TC_DIAG_LANE_SEL = 46,
+    TC_DIAG_UNIFORM = 47,   // target on a warp / outer qubit
+    TC_DIAG_UNIFORM_SEL = 48,
+    TC_DEPHASE = 49,
+    TC_COLLAPSE = 50,
 };
 
 // Op header packed in one 64-bit word (one constant-bank load per op):
@@ -142,9 +150,6 @@ struct TilePhase {
     uint16_t reg_off[1 << kPhaseRegBits];  // tile index of register i (lane 0, warp 0)
     uint16_t warp_off[1 << kTileWarpBits]; // tile index offset of warp w
     uint16_t op_begin, op_end;
-    // index of the (single) register-pair op on register bit j, 0xFFFF if
-    // none; increasing in j (kernels.cu: run_phase_ops)
-    uint16_t reg_at[kPhaseRegBits];
 };
 
 struct TileParams {

@@ -213,17 +213,16 @@ bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
         const int q = op.q0;
         const bool in_tile = std::find(tile_high.begin(), tile_high.end(), q) != tile_high.end();
         if (!in_tile && static_cast<int>(tile_high.size()) >= kTileHigh) return false;
-        // one register op per register bit per phase (kernels.cu: run_phase_ops)
+        // a phase holds kPhaseRegBits register qubits
         PhaseState& ph = phases.back();
         const bool in_phase = std::find(ph.regs.begin(), ph.regs.end(), q) != ph.regs.end();
-        if (in_phase || static_cast<int>(ph.regs.size()) >= kPhaseRegBits) {
+        if (!in_phase && static_cast<int>(ph.regs.size()) >= kPhaseRegBits) {
             if (static_cast<int>(phases.size()) >= kMaxPhases) return false;
             PhaseState next;
             next.op_begin = static_cast<int>(pending.size());
             phases.push_back(next);
         }
-        phases.back().regs.push_back(q);
-        phases.back().reg_ops.push_back(static_cast<int>(pending.size()));
+        if (!in_phase) phases.back().regs.push_back(q);
         if (!in_tile) tile_high.push_back(q);
     }
     pending.push_back(op);
@@ -331,10 +330,6 @@ void QuregImpl::launch_tile() {
         const int end = p + 1 < phases.size() ? phases[p + 1].op_begin : static_cast<int>(pending.size());
         Q.op_begin = static_cast<uint16_t>(begin);
         Q.op_end = static_cast<uint16_t>(end);
-        for (int j = 0; j < kPhaseRegBits; ++j)
-            Q.reg_at[j] = j < static_cast<int>(phases[p].reg_ops.size())
-                              ? static_cast<uint16_t>(phases[p].reg_ops[j])
-                              : uint16_t{0xFFFF};
         auto loc = [&](int q, uint8_t* kind, uint8_t* pos) {
             const int t = tbit(q);
             if (q < 0) {
@@ -380,15 +375,27 @@ void QuregImpl::launch_tile() {
                 if (ck == TL_REG) reg_cm |= 1u << cp;
                 if (ck == TL_WARP) warp_cm |= 1u << cp;
             }
-            // resolve the kernel's handler (qgpu_device.h: TileCode)
-            const bool ctrl = op.cmask != 0;
+            // resolve the kernel's handler (qgpu_device.h: TileCode); lane,
+            // register and warp controls need the per-element predicate (SEL
+            // codes), outer controls skip the op per tile
+            const bool ctrl = lane_cm != 0 || reg_cm != 0 || warp_cm != 0;
             uint32_t code;
             if (op.kind == FK_DEPHASE) {
                 code = TC_DEPHASE;
             } else if (op.kind == FK_COLLAPSE) {
                 code = TC_COLLAPSE;
             } else if (op.cls == CLS_DIAG) {
-                code = q0k == TL_REG ? TC_DIAG_REG + q0p : TC_DIAG_FIXED;
+                if (q0k == TL_REG) {
+                    // a == 1 exactly: the low side is the identity (a * v
+                    // with a = 1 + 0i rounds to v), leave it alone
+                    const bool d_only = (op.flags & DF_A_ONE) != 0;
+                    code = (ctrl ? (d_only ? TC_DIAG_REG_D_SEL : TC_DIAG_REG_SEL)
+                                 : (d_only ? TC_DIAG_REG_D : TC_DIAG_REG)) + q0p;
+                } else if (q0k == TL_LANE) {
+                    code = ctrl ? TC_DIAG_LANE_SEL : TC_DIAG_LANE;
+                } else {
+                    code = ctrl ? TC_DIAG_UNIFORM_SEL : TC_DIAG_UNIFORM;
+                }
             } else if (q0k == TL_LANE) {
                 if (!ctrl)
                     code = op.cls == CLS_SWAP   ? TC_LANE_SWAP

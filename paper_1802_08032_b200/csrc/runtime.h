@@ -119,8 +119,7 @@ struct QuregImpl {
     std::vector<FlatOp> pending;
     std::vector<int> regs; // register qubits (small-state register pass)
     struct PhaseState {
-        std::vector<int> regs;    // register qubits, in order of their (single) op
-        std::vector<int> reg_ops; // index of that op in `pending`
+        std::vector<int> regs; // register qubits of the phase
         int op_begin = 0;
     };
     std::vector<int> tile_high;      // tile pass: high qubits in the tile

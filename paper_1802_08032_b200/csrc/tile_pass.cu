@@ -4,22 +4,27 @@
 // Structure (qgpu_device.h: TileParams / TilePhase / TileOp):
 //  * one persistent CTA per SM walks tiles of 2^12 amplitudes (qubits 0-4 plus
 //    7 higher qubits chosen per pass);
-//  * HBM <-> shared memory through TMA: warp 0 issues cp.async.bulk loads of
-//    tile t+1 (completion on an mbarrier) and bulk stores of tile t, three
-//    64 KiB stages deep, so the streaming overlaps the ops on the current tile
-//    and no register holds data in flight;
-//  * the ops run in phases: every thread holds 16 amplitudes in registers
-//    spanning the phase's 4 register qubits (lanes span qubits 0-4, the 8
-//    warps the remaining 3 tile qubits). Pair ops on register qubits stay in
-//    registers, on lane qubits they use warp shuffles, diagonal gates and
-//    channels are elementwise anywhere; between phases the tile is re-laid out
-//    through shared memory.
+//  * HBM <-> shared memory through TMA: warp 0 issues cp.async.bulk loads
+//    (completion on an mbarrier) and bulk stores at tile boundaries, three
+//    64 KiB stages deep, so the streaming overlaps the ops and no register
+//    holds data in flight;
+//  * the ops run in phases: every consumer thread holds 16 amplitudes in
+//    registers spanning the phase's 4 register qubits (lanes span qubits 0-4,
+//    the 8 consumer warps the remaining 3 tile qubits). Pair ops on register
+//    qubits stay in registers, on lane qubits they use warp shuffles, diagonal
+//    gates and channels are elementwise anywhere; between phases the tile is
+//    re-laid out through shared memory.
 //
-// Register discipline: each op reads one register array and writes every
-// element of the other (the op loop alternates A -> B, B -> A). Updating one
-// array in place made ptxas copy the whole 64-register tile on every op
-// (ncu: IMAD.MOV = 45% of issued instructions); with disjoint source and
-// destination each result is computed straight into its final register.
+// Code-generation notes (each measured with ncu on this kernel):
+//  * the op table is copied to shared memory once per launch — read from the
+//    kernel-parameter bank every op missed the constant cache;
+//  * an op's header and coefficients are loaded one op ahead (OpCtx), so their
+//    latency hides behind the previous op;
+//  * the host resolves each op to one handler code (TileCode): one jump table;
+//  * handlers never branch per element on run-time values (selects only where
+//    lane / register controls need them) — per-element branches made ptxas
+//    copy the whole 64-register tile around them;
+//  * warp-uniform controls (on warp or outer qubits) skip the op outright.
 #include "pair_math.cuh"
 #include "qgpu_kernels.h"
 #include "runtime.h"
@@ -48,6 +53,10 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -92,9 +101,13 @@ __device__ __forceinline__ void fence_proxy_async() {
 
 // ---------------------------------------------------------------- handlers
 //
-// Every handler reads `s` and writes all of `d`. SEL variants apply a
-// per-element predicate (controls on register bits `rcm`, or on lane bits via
-// `tok`); the common, uncontrolled variants have none.
+// Ping-pong: every handler reads the tile s and writes every element of the
+// tile d (a fresh register set), so the results of all switch arms land in
+// the same registers with no copies; the op loop alternates s and d. (An
+// in-place update leaves each pair's results in rotated registers, and ptxas
+// then copies the whole tile back at every loop iteration: measured 30 %
+// slower.) SEL variants apply a per-element predicate: register controls
+// `rcm` and lane controls (`tok`).
 
 __device__ __forceinline__ double2 diag_a(const double* c, double2 v) {
     return make_double2(fma(c[0], v.x, -(c[1] * v.y)), fma(c[0], v.y, c[1] * v.x));
@@ -103,54 +116,28 @@ __device__ __forceinline__ double2 diag_d(const double* c, double2 v) {
     return make_double2(fma(-c[7], v.y, c[6] * v.x), fma(c[7], v.x, c[6] * v.y));
 }
 
-template <int RB>
-__device__ __forceinline__ void h_copy(const Regs<RB>& s, Regs<RB>& d) {
-#pragma unroll
-    for (int i = 0; i < (1 << RB); ++i) d[i] = s[i];
+__device__ __forceinline__ bool sel_on(int i, uint32_t rcm, bool tok) {
+    return tok && (static_cast<uint32_t>(i) & rcm) == rcm;
 }
 
-// 2x2 gate on register bit J (compile time): lo = i with bit J clear.
+// 2x2 gate on register bit J (compile time).
 template <int RB, int J, int CLS, bool SEL>
-__device__ __forceinline__ void h_reg_pair(const Regs<RB>& s, Regs<RB>& d, const double* c,
-                                           uint32_t rcm, bool tok) {
-#pragma unroll
-    for (int i = 0; i < (1 << RB); ++i) {
-        constexpr int bit = 1 << J;
-        const int lo = i & ~bit, hi = i | bit;
-        double2 r;
-        if constexpr (CLS == CLS_SWAP)
-            r = s[i ^ bit];
-        else if (i & bit)
-            r = row<ClassZ<CLS>::z1>(c[4], c[5], c[6], c[7], s[lo], s[hi]);
-        else
-            r = row<ClassZ<CLS>::z0>(c[0], c[1], c[2], c[3], s[lo], s[hi]);
-        if constexpr (SEL) {
-            const bool on = tok && (static_cast<uint32_t>(lo) & rcm) == rcm;
-            d[i] = on ? r : s[i];
-        } else {
-            d[i] = r;
-        }
-    }
-}
-
-// In-place form of h_reg_pair (one array): pair by pair, both outputs are
-// computed before either input is overwritten.
-template <int RB, int J, int CLS, bool SEL>
-__device__ __forceinline__ void h_reg_pair_ip(Regs<RB>& v, const double* c, uint32_t rcm, bool tok) {
+__device__ __forceinline__ void h_reg(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t rcm,
+                                      bool tok) {
     if constexpr (J < RB) {
 #pragma unroll
         for (int lo = 0; lo < (1 << RB); ++lo) {
             constexpr int bit = 1 << J;
             if (lo & bit) continue;
-            double2 l = v[lo], h = v[lo | bit];
+            double2 l = s[lo], h = s[lo | bit];
             pair_update<CLS>(l, h, c);
             if constexpr (SEL) {
-                const bool on = tok && (static_cast<uint32_t>(lo) & rcm) == rcm;
-                v[lo] = on ? l : v[lo];
-                v[lo | bit] = on ? h : v[lo | bit];
+                const bool on = sel_on(lo, rcm, tok);
+                d[lo] = on ? l : s[lo];
+                d[lo | bit] = on ? h : s[lo | bit];
             } else {
-                v[lo] = l;
-                v[lo | bit] = h;
+                d[lo] = l;
+                d[lo | bit] = h;
             }
         }
     }
@@ -160,8 +147,8 @@ __device__ __forceinline__ void h_reg_pair_ip(Regs<RB>& v, const double* c, uint
 // each lane computes its own half (distributed.cpp:183-184:
 // own_lo ? lo_out(mine, theirs) : hi_out(theirs, mine)).
 template <int RB, int CLS, bool SEL>
-__device__ __forceinline__ void h_lane_pair(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t b,
-                                            uint32_t rcm, bool tok, uint32_t lane) {
+__device__ __forceinline__ void h_lane(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t b,
+                                       uint32_t rcm, bool tok, uint32_t lane) {
     const uint32_t mask = 1u << b;
     const bool own_lo = (lane & mask) == 0;
     const double q0 = own_lo ? c[0] : c[4], q1 = own_lo ? c[1] : c[5];
@@ -179,49 +166,81 @@ __device__ __forceinline__ void h_lane_pair(const Regs<RB>& s, Regs<RB>& d, cons
             const double2 hi = own_lo ? th : s[i];
             r = row<CLS == CLS_REAL ? 0b1010 : 0>(q0, q1, q2, q3, lo, hi);
         }
-        if constexpr (SEL) {
-            const bool on = tok && (static_cast<uint32_t>(i) & rcm) == rcm;
-            d[i] = on ? r : s[i];
-        } else {
+        if constexpr (SEL)
+            d[i] = sel_on(i, rcm, tok) ? r : s[i];
+        else
             d[i] = r;
+    }
+}
+
+// Diagonal gate, target on register bit J: a * v where the bit is 0, d * v
+// where it is 1 (rounding of the reference's low / high row). DO_A = false
+// leaves the low side alone (a == 1 exactly).
+template <int RB, int J, bool DO_A, bool SEL>
+__device__ __forceinline__ void h_diag_reg(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t rcm,
+                                           bool tok) {
+    if constexpr (J < RB) {
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i) {
+            const bool bit = (i >> J) & 1;
+            if (!bit && !DO_A) { // compile time
+                d[i] = s[i];
+                continue;
+            }
+            const double2 r = bit ? diag_d(c, s[i]) : diag_a(c, s[i]);
+            if constexpr (SEL)
+                d[i] = sel_on(i, rcm, tok) ? r : s[i];
+            else
+                d[i] = r;
         }
     }
 }
 
-// Diagonal gate with its target on register bit J: a * v where the bit is 0,
-// d * v where it is 1 (rounding of the reference's low / high row). A side
-// whose coefficient is exactly 1 keeps its input (flags).
-template <int RB, int J>
-__device__ __forceinline__ void h_diag_reg(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t rcm,
-                                           bool tok, bool a_one, bool d_one) {
-#pragma unroll
-    for (int i = 0; i < (1 << RB); ++i) {
-        const bool bit = (i >> J) & 1;
-        const double2 r = bit ? diag_d(c, s[i]) : diag_a(c, s[i]);
-        const bool on = tok && !(bit ? d_one : a_one) && (static_cast<uint32_t>(i) & rcm) == rcm;
-        d[i] = on ? r : s[i];
-    }
-}
-
-// Diagonal gate whose target bit is fixed for this thread (lane, warp or
-// outer qubit): coefficients picked once; per element the operands swap:
+// Diagonal gate whose target bit differs per lane: coefficients picked once
+// per thread; per element the operands swap:
 //   re = fma(P, X, Q * Y), im = fma(R, Y, S * X)
-//   bit 0: P = a_re, Q = -a_im, R = a_re, S = a_im, (X, Y) = (x, y)
-//   bit 1: P = -d_im, Q = d_re, R = d_im, S = d_re, (X, Y) = (y, x)
-template <int RB>
-__device__ __forceinline__ void h_diag_fixed(const Regs<RB>& s, Regs<RB>& d, const double* c,
-                                             uint32_t bit, uint32_t rcm, bool tok, bool a_one,
-                                             bool d_one) {
+//   bit 0: P = a_re, Q = -a_im, R = a_re, S = a_im, (X, Y) = (x, y)   (diag_a)
+//   bit 1: P = -d_im, Q = d_re, R = d_im, S = d_re, (X, Y) = (y, x)   (diag_d)
+template <int RB, bool SEL>
+__device__ __forceinline__ void h_diag_lane(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t bit,
+                                            uint32_t rcm, bool tok) {
     const double P = bit ? -c[7] : c[0], Q = bit ? c[6] : -c[1];
     const double R = bit ? c[7] : c[0], S = bit ? c[6] : c[1];
-    const bool doit = tok && !(bit ? d_one : a_one);
 #pragma unroll
     for (int i = 0; i < (1 << RB); ++i) {
         const double X = bit ? s[i].y : s[i].x, Y = bit ? s[i].x : s[i].y;
         const double2 r = make_double2(fma(P, X, Q * Y), fma(R, Y, S * X));
-        const bool on = doit && (static_cast<uint32_t>(i) & rcm) == rcm;
-        d[i] = on ? r : s[i];
+        if constexpr (SEL)
+            d[i] = sel_on(i, rcm, tok) ? r : s[i];
+        else
+            d[i] = r;
     }
+}
+
+// Diagonal gate whose target bit is the same for the whole warp (a warp or
+// outer qubit): a warp-uniform branch picks the side.
+template <int RB, bool SEL>
+__device__ __forceinline__ void h_diag_uniform(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t bit,
+                                               uint32_t rcm, bool tok) {
+    if (bit) {
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i) {
+            const double2 r = diag_d(c, s[i]);
+            d[i] = SEL ? (sel_on(i, rcm, tok) ? r : s[i]) : r;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < (1 << RB); ++i) {
+            const double2 r = diag_a(c, s[i]);
+            d[i] = SEL ? (sel_on(i, rcm, tok) ? r : s[i]) : r;
+        }
+    }
+}
+
+template <int RB>
+__device__ __forceinline__ void h_copy(const Regs<RB>& s, Regs<RB>& d) {
+#pragma unroll
+    for (int i = 0; i < (1 << RB); ++i) d[i] = s[i];
 }
 
 __device__ __forceinline__ uint32_t fixed_bit_of(uint32_t kind, uint32_t pos, uint32_t lane, uint32_t w,
@@ -231,77 +250,106 @@ __device__ __forceinline__ uint32_t fixed_bit_of(uint32_t kind, uint32_t pos, ui
                              : static_cast<uint32_t>((gbase >> pos) & 1u);
 }
 
-// One op: s -> d. `h` is the op's header, loaded by the caller one op ahead
-// so its constant-bank latency hides behind the previous op; its low 6 bits
-// are the handler code the host resolved (qgpu_device.h: TileCode), so
-// dispatch is a single jump table.
-template <int RB, bool IP, int J, int CLS, bool SEL>
-__device__ __forceinline__ void reg_op(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t rcm,
-                                       bool tok) {
-    if constexpr (J < RB) {
-        if constexpr (IP)
-            h_reg_pair_ip<RB, J, CLS, SEL>(d, c, rcm, tok);
-        else
-            h_reg_pair<RB, J, CLS, SEL>(s, d, c, rcm, tok);
-    }
+// An op's header and coefficients, loaded one op ahead.
+struct OpCtx {
+    uint64_t h;
+    double c[8];
+};
+
+__device__ __forceinline__ void load_ctx(OpCtx& x, const TileOp& op) {
+    x.h = op.hdr;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x.c[k] = op.m[k];
 }
 
-// IP (in place): s and d are the same array; every handler but the register
-// pairs is elementwise (reads element i before writing it), so only those
-// switch to their pairwise in-place form.
-template <int RB, bool IP>
-__device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, uint64_t h, const TileOp& op,
-                                     uint32_t lane, uint32_t w, uint64_t gbase) {
-    static_assert(RB <= 4, "register-bit dispatch is written for up to 4 register qubits");
-    const uint32_t code = h & 63u, flags = (h >> 6) & 15u;
-    const uint32_t q0k = (h >> 11) & 3u, q0p = (h >> 13) & 63u;
+// Controls on outer qubits are uniform per tile: such an op is skipped by the
+// whole CTA (the op loop never visits it). Controls on warp qubits are not
+// skipped but folded into the per-element predicate like lane / register
+// ones: a warp that skipped would idle at the next phase barrier while its
+// sub-partition ran the other warp alone (measured: 32 % barrier stalls).
+__device__ __forceinline__ int next_active(const TileOp* ops, int o, int end, uint64_t gbase) {
+    while (o < end && (gbase & ops[o].outer_cmask) != ops[o].outer_cmask) ++o;
+    return o;
+}
+
+// One op: s -> d.
+template <int RB>
+__device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, const OpCtx& x, uint32_t lane,
+                                     uint32_t w, uint64_t gbase) {
+    const uint64_t h = x.h;
+    const uint32_t code = h & 63u;
+    const uint32_t q0p = (h >> 13) & 63u;
     const uint32_t lane_cm = (h >> 27) & 31u, rcm = (h >> 32) & 15u, warp_cm = (h >> 36) & 15u;
-    const uint64_t ocm = op.outer_cmask;
-    // Controls fold into one per-thread predicate. (A separate early-out that
-    // copied s to d for a failing warp made ptxas hoist that whole-tile copy
-    // above the branch, i.e. onto every op.)
-    const bool tok = (lane & lane_cm) == lane_cm && (w & warp_cm) == warp_cm && (gbase & ocm) == ocm;
-    const bool a_one = flags & DF_A_ONE, d_one = flags & DF_D_ONE;
-    const double* c = op.m; // coefficients are read from the constant bank where used
+    const bool tok = (lane & lane_cm) == lane_cm && (w & warp_cm) == warp_cm;
+    const double* c = x.c;
     switch (code) {
-    case TC_REG + 0: reg_op<RB, IP,0, CLS_GENERIC, false>(s, d, c, 0, true); break;
-    case TC_REG + 1: reg_op<RB, IP,1, CLS_GENERIC, false>(s, d, c, 0, true); break;
-    case TC_REG + 2: reg_op<RB, IP,2, CLS_GENERIC, false>(s, d, c, 0, true); break;
-    case TC_REG + 3: reg_op<RB, IP,3, CLS_GENERIC, false>(s, d, c, 0, true); break;
-    case TC_REG + 4: reg_op<RB, IP,0, CLS_REAL, false>(s, d, c, 0, true); break;
-    case TC_REG + 5: reg_op<RB, IP,1, CLS_REAL, false>(s, d, c, 0, true); break;
-    case TC_REG + 6: reg_op<RB, IP,2, CLS_REAL, false>(s, d, c, 0, true); break;
-    case TC_REG + 7: reg_op<RB, IP,3, CLS_REAL, false>(s, d, c, 0, true); break;
-    case TC_REG + 8: reg_op<RB, IP,0, CLS_RX, false>(s, d, c, 0, true); break;
-    case TC_REG + 9: reg_op<RB, IP,1, CLS_RX, false>(s, d, c, 0, true); break;
-    case TC_REG + 10: reg_op<RB, IP,2, CLS_RX, false>(s, d, c, 0, true); break;
-    case TC_REG + 11: reg_op<RB, IP,3, CLS_RX, false>(s, d, c, 0, true); break;
-    case TC_REG + 12: reg_op<RB, IP,0, CLS_SWAP, false>(s, d, c, 0, true); break;
-    case TC_REG + 13: reg_op<RB, IP,1, CLS_SWAP, false>(s, d, c, 0, true); break;
-    case TC_REG + 14: reg_op<RB, IP,2, CLS_SWAP, false>(s, d, c, 0, true); break;
-    case TC_REG + 15: reg_op<RB, IP,3, CLS_SWAP, false>(s, d, c, 0, true); break;
-    case TC_REG_SEL + 0: reg_op<RB, IP,0, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 1: reg_op<RB, IP,1, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 2: reg_op<RB, IP,2, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 3: reg_op<RB, IP,3, CLS_GENERIC, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 4: reg_op<RB, IP,0, CLS_SWAP, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 5: reg_op<RB, IP,1, CLS_SWAP, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 6: reg_op<RB, IP,2, CLS_SWAP, true>(s, d, c, rcm, tok); break;
-    case TC_REG_SEL + 7: reg_op<RB, IP,3, CLS_SWAP, true>(s, d, c, rcm, tok); break;
-    case TC_LANE_GENERIC: h_lane_pair<RB, CLS_GENERIC, false>(s, d, c, q0p, 0, true, lane); break;
-    case TC_LANE_REAL: h_lane_pair<RB, CLS_REAL, false>(s, d, c, q0p, 0, true, lane); break;
-    case TC_LANE_SWAP: h_lane_pair<RB, CLS_SWAP, false>(s, d, c, q0p, 0, true, lane); break;
-    case TC_LANE_SEL_GENERIC: h_lane_pair<RB, CLS_GENERIC, true>(s, d, c, q0p, rcm, tok, lane); break;
-    case TC_LANE_SEL_SWAP: h_lane_pair<RB, CLS_SWAP, true>(s, d, c, q0p, rcm, tok, lane); break;
-    case TC_DIAG_REG + 0: h_diag_reg<RB, 0>(s, d, c, rcm, tok, a_one, d_one); break;
-    case TC_DIAG_REG + 1: h_diag_reg<RB, 1>(s, d, c, rcm, tok, a_one, d_one); break;
-    case TC_DIAG_REG + 2: h_diag_reg<RB, 2>(s, d, c, rcm, tok, a_one, d_one); break;
-    case TC_DIAG_REG + 3: h_diag_reg<RB, 3>(s, d, c, rcm, tok, a_one, d_one); break;
-    case TC_DIAG_FIXED:
-        h_diag_fixed<RB>(s, d, c, fixed_bit_of(q0k, q0p, lane, w, gbase), rcm, tok, a_one, d_one);
+#define QGPU_REG(CODE, J, CLS, SEL)                                \
+    case CODE: h_reg<RB, J, CLS, SEL>(s, d, c, rcm, tok); break;
+        QGPU_REG(TC_REG + 0, 0, CLS_GENERIC, false)
+        QGPU_REG(TC_REG + 1, 1, CLS_GENERIC, false)
+        QGPU_REG(TC_REG + 2, 2, CLS_GENERIC, false)
+        QGPU_REG(TC_REG + 3, 3, CLS_GENERIC, false)
+        QGPU_REG(TC_REG + 4, 0, CLS_REAL, false)
+        QGPU_REG(TC_REG + 5, 1, CLS_REAL, false)
+        QGPU_REG(TC_REG + 6, 2, CLS_REAL, false)
+        QGPU_REG(TC_REG + 7, 3, CLS_REAL, false)
+        QGPU_REG(TC_REG + 8, 0, CLS_RX, false)
+        QGPU_REG(TC_REG + 9, 1, CLS_RX, false)
+        QGPU_REG(TC_REG + 10, 2, CLS_RX, false)
+        QGPU_REG(TC_REG + 11, 3, CLS_RX, false)
+        QGPU_REG(TC_REG + 12, 0, CLS_SWAP, false)
+        QGPU_REG(TC_REG + 13, 1, CLS_SWAP, false)
+        QGPU_REG(TC_REG + 14, 2, CLS_SWAP, false)
+        QGPU_REG(TC_REG + 15, 3, CLS_SWAP, false)
+        QGPU_REG(TC_REG_SEL + 0, 0, CLS_GENERIC, true)
+        QGPU_REG(TC_REG_SEL + 1, 1, CLS_GENERIC, true)
+        QGPU_REG(TC_REG_SEL + 2, 2, CLS_GENERIC, true)
+        QGPU_REG(TC_REG_SEL + 3, 3, CLS_GENERIC, true)
+        QGPU_REG(TC_REG_SEL + 4, 0, CLS_SWAP, true)
+        QGPU_REG(TC_REG_SEL + 5, 1, CLS_SWAP, true)
+        QGPU_REG(TC_REG_SEL + 6, 2, CLS_SWAP, true)
+        QGPU_REG(TC_REG_SEL + 7, 3, CLS_SWAP, true)
+#undef QGPU_REG
+    case TC_LANE_GENERIC: h_lane<RB, CLS_GENERIC, false>(s, d, c, q0p, 0, true, lane); break;
+    case TC_LANE_REAL: h_lane<RB, CLS_REAL, false>(s, d, c, q0p, 0, true, lane); break;
+    case TC_LANE_SWAP: h_lane<RB, CLS_SWAP, false>(s, d, c, q0p, 0, true, lane); break;
+    case TC_LANE_SEL_GENERIC: h_lane<RB, CLS_GENERIC, true>(s, d, c, q0p, rcm, tok, lane); break;
+    case TC_LANE_SEL_SWAP: h_lane<RB, CLS_SWAP, true>(s, d, c, q0p, rcm, tok, lane); break;
+#define QGPU_DIAG(CODE, J, DA, SEL)                                \
+    case CODE: h_diag_reg<RB, J, DA, SEL>(s, d, c, rcm, tok); break;
+        QGPU_DIAG(TC_DIAG_REG + 0, 0, true, false)
+        QGPU_DIAG(TC_DIAG_REG + 1, 1, true, false)
+        QGPU_DIAG(TC_DIAG_REG + 2, 2, true, false)
+        QGPU_DIAG(TC_DIAG_REG + 3, 3, true, false)
+        QGPU_DIAG(TC_DIAG_REG_D + 0, 0, false, false)
+        QGPU_DIAG(TC_DIAG_REG_D + 1, 1, false, false)
+        QGPU_DIAG(TC_DIAG_REG_D + 2, 2, false, false)
+        QGPU_DIAG(TC_DIAG_REG_D + 3, 3, false, false)
+        QGPU_DIAG(TC_DIAG_REG_SEL + 0, 0, true, true)
+        QGPU_DIAG(TC_DIAG_REG_SEL + 1, 1, true, true)
+        QGPU_DIAG(TC_DIAG_REG_SEL + 2, 2, true, true)
+        QGPU_DIAG(TC_DIAG_REG_SEL + 3, 3, true, true)
+        QGPU_DIAG(TC_DIAG_REG_D_SEL + 0, 0, false, true)
+        QGPU_DIAG(TC_DIAG_REG_D_SEL + 1, 1, false, true)
+        QGPU_DIAG(TC_DIAG_REG_D_SEL + 2, 2, false, true)
+        QGPU_DIAG(TC_DIAG_REG_D_SEL + 3, 3, false, true)
+#undef QGPU_DIAG
+    case TC_DIAG_LANE: h_diag_lane<RB, false>(s, d, c, (lane >> q0p) & 1u, 0, true); break;
+    case TC_DIAG_LANE_SEL: h_diag_lane<RB, true>(s, d, c, (lane >> q0p) & 1u, rcm, tok); break;
+    case TC_DIAG_UNIFORM:
+    case TC_DIAG_UNIFORM_SEL: {
+        const uint32_t flags = (h >> 6) & 15u;
+        const uint32_t bit = fixed_bit_of((h >> 11) & 3u, q0p, lane, w, gbase);
+        if (bit ? (flags & DF_D_ONE) : (flags & DF_A_ONE)) // identity side
+            h_copy<RB>(s, d);
+        else if (code == TC_DIAG_UNIFORM)
+            h_diag_uniform<RB, false>(s, d, c, bit, 0, true);
+        else
+            h_diag_uniform<RB, true>(s, d, c, bit, rcm, tok);
         break;
+    }
     case TC_DEPHASE: { // density.cpp:56-59: scale where bit(q0) != bit(q1)
-        const uint32_t q1k = (h >> 19) & 3u, q1p = (h >> 21) & 63u;
+        const uint32_t q0k = (h >> 11) & 3u, q1k = (h >> 19) & 3u, q1p = (h >> 21) & 63u;
         const uint32_t rm = (q0k == TL_REG ? 1u << q0p : 0u) ^ (q1k == TL_REG ? 1u << q1p : 0u);
         const uint32_t f = (q0k == TL_REG ? 0u : fixed_bit_of(q0k, q0p, lane, w, gbase)) ^
                            (q1k == TL_REG ? 0u : fixed_bit_of(q1k, q1p, lane, w, gbase));
@@ -314,8 +362,9 @@ __device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, uint64_t h,
         }
         break;
     }
-    default: { // PO_COLLAPSE: keep bit(q0) (and bit(q1)) == outcome, scaled
-        const uint32_t q1k = (h >> 19) & 3u, q1p = (h >> 21) & 63u;
+    case TC_COLLAPSE: { // keep bit(q0) (and bit(q1)) == outcome, scaled
+        const uint32_t flags = (h >> 6) & 15u;
+        const uint32_t q0k = (h >> 11) & 3u, q1k = (h >> 19) & 3u, q1p = (h >> 21) & 63u;
         const uint32_t o = (h >> 10) & 1u;
         const bool two = flags & 1;
         const bool r0 = q0k == TL_REG, r1 = q1k == TL_REG;
@@ -331,6 +380,7 @@ __device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, uint64_t h,
         }
         break;
     }
+    default: __builtin_unreachable(); // the host emits TileCode values only
     }
 }
 
@@ -342,140 +392,119 @@ __device__ __forceinline__ uint64_t tile_gbase(const TileParams& P, uint64_t T) 
     return gb;
 }
 
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-// Named barrier among the consumer warps only (the producer never joins).
-template <int NTHREADS>
-__device__ __forceinline__ void consumer_sync() {
-    asm volatile("bar.sync 1, %0;" ::"n"(NTHREADS) : "memory");
-}
-
-// Warp-specialised: warps 0 .. 2^WB - 1 apply the ops, the last warp is the
-// TMA producer. full[b]: stage b holds a loaded tile (tx-count barrier).
-// done[b]: the consumers have written stage b's last phase (one arrival per
-// consumer warp); the producer then bulk-stores it and, once the store has
-// read the stage, refills it with the tile NBUF ahead.
-template <int RB, int WB, int NBUF, bool INPLACE>
-__global__ void __launch_bounds__((32 << WB) + 32, 1) // 9 warps: <= 168 registers
+// All 2^WB warps apply the ops and share the TMA copies at tile boundaries
+// (one bulk copy per thread: a single issuing warp made the others wait at
+// the next phase barrier, 33 % of all stall samples). full[b]: stage b holds
+// a loaded tile (tx-count barrier). After the block barrier that ends tile t,
+// the threads bulk-store stage t % NBUF and refill the stage freed one tile
+// earlier with tile t - 1 + NBUF; each thread waited for its own part of that
+// stage's store to leave shared memory before the barrier, long after it was
+// issued, so the wait never stalls. No separate producer warp: 8 warps (2 per
+// SM sub-partition) may use 255 registers each, where a 9th warp would cap
+// them at 168.
+template <int RB, int WB, int NBUF>
+__global__ void __launch_bounds__(32 << WB, 1)
 k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
     constexpr int R = 1 << RB;
     constexpr int K = kLaneQubits + RB + WB;
     constexpr int NSEG = 1 << (RB + WB);
-    constexpr int NCW = 1 << WB; // consumer warps
     constexpr uint32_t TILE_BYTES = sizeof(double2) << K;
     extern __shared__ __align__(128) double2 smem[];
-    __shared__ uint64_t full[NBUF], done[NBUF];
+    __shared__ TileOp sops[kMaxTileOps + 1]; // + 1: the prefetch may read one past
+    __shared__ uint64_t full[NBUF];
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t w = threadIdx.x >> 5;
     const int nph = P.num_phases;
     const uint64_t G = gridDim.x;
     const uint64_t ntiles = P.num_tiles > blockIdx.x ? (P.num_tiles - blockIdx.x + G - 1) / G : 0;
 
-    if (threadIdx.x == 0) {
-        for (int b = 0; b < NBUF; ++b) {
-            mbar_init(&full[b], 1);
-            mbar_init(&done[b], NCW);
+    // runs of 2^seg_run segments are contiguous in HBM: one bulk copy each,
+    // spread over the threads. The expected byte count may be posted after
+    // other threads' copies completed: the tx-count goes negative meanwhile
+    // and the phase cannot complete before thread 0's arrival.
+    const int run = P.seg_run;
+    auto copies = [&](uint64_t t, bool load) {
+        const int b = static_cast<int>(t % NBUF);
+        const uint64_t gb = tile_gbase<RB, WB>(P, blockIdx.x + t * G);
+        double2* buf = smem + (static_cast<size_t>(b) << K);
+        if (load && threadIdx.x == 0) mbar_expect_tx(&full[b], TILE_BYTES);
+        for (int sg = static_cast<int>(threadIdx.x) << run; sg < NSEG; sg += blockDim.x << run) {
+            if (load)
+                tma_load(buf + (sg << kLaneQubits), amps + gb + P.seg_off[sg],
+                         (32u * sizeof(double2)) << run, &full[b]);
+            else
+                tma_store(amps + gb + P.seg_off[sg], buf + (sg << kLaneQubits),
+                          (32u * sizeof(double2)) << run);
         }
+    };
+
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < NBUF; ++b) mbar_init(&full[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncthreads();
-
-    if (w == NCW) { // ---------------------------------------------- producer
-        // runs of 2^seg_run segments are contiguous in HBM: one bulk copy each
-        const int run = P.seg_run;
-        auto copies = [&](uint64_t t, bool load) {
-            const int b = static_cast<int>(t % NBUF);
-            const uint64_t gb = tile_gbase<RB, WB>(P, blockIdx.x + t * G);
-            double2* buf = smem + (static_cast<size_t>(b) << K);
-            for (int sg = lane << run; sg < NSEG; sg += 32 << run) {
-                if (load)
-                    tma_load(buf + (sg << kLaneQubits), amps + gb + P.seg_off[sg],
-                             (32u * sizeof(double2)) << run, &full[b]);
-                else
-                    tma_store(amps + gb + P.seg_off[sg], buf + (sg << kLaneQubits),
-                              (32u * sizeof(double2)) << run);
-            }
-        };
-        auto store = [&](uint64_t t) {
-            mbar_wait(&done[t % NBUF], static_cast<uint32_t>((t / NBUF) & 1));
-            copies(t, false);
-            tma_commit();
-        };
-        for (uint64_t t = 0; t < ntiles; ++t) {
-            if (t >= NBUF) { // stage t % NBUF still holds tile t - NBUF
-                store(t - NBUF);
-                tma_wait_read<0>();
-                __syncwarp();
-            }
-            if (lane == 0) mbar_expect_tx(&full[t % NBUF], TILE_BYTES);
-            __syncwarp();
-            copies(t, true);
-        }
-        for (uint64_t t = ntiles > NBUF ? ntiles - NBUF : 0; t < ntiles; ++t) store(t);
-        tma_wait_all();
-        return;
+    for (uint64_t t = 0; t < NBUF && t < ntiles; ++t) copies(t, true);
+    {
+        const int nops = P.phases[nph - 1].op_end;
+        const uint64_t* src = reinterpret_cast<const uint64_t*>(P.ops);
+        uint64_t* dst = reinterpret_cast<uint64_t*>(sops);
+        constexpr int WORDS = sizeof(TileOp) / sizeof(uint64_t);
+        for (int k = threadIdx.x; k < nops * WORDS; k += blockDim.x) dst[k] = src[k];
     }
+    __syncthreads();
 
-    // ------------------------------------------------------------ consumers
     for (uint64_t t = 0; t < ntiles; ++t) {
         const int b = static_cast<int>(t % NBUF);
         double2* buf = smem + (static_cast<size_t>(b) << K);
         const uint64_t gbase = tile_gbase<RB, WB>(P, blockIdx.x + t * G) + P.global_offset;
         mbar_wait(&full[b], static_cast<uint32_t>((t / NBUF) & 1));
         for (int ph = 0; ph < nph; ++ph) {
-            if (ph > 0) consumer_sync<32 * NCW>(); // previous phase's writes are in
+            if (ph > 0) __syncthreads(); // previous phase's writes are in
             const TilePhase& Q = P.phases[ph];
             const uint32_t wofs = Q.warp_off[w] + lane;
+            double2 a[R], b[R];
+#pragma unroll
+            for (int i = 0; i < R; ++i) a[i] = buf[wofs + Q.reg_off[i]];
+            // ops alternate a -> b, b -> a; the contexts alternate too, each
+            // loaded one op ahead (sops has a spare entry past the last op)
             const int end = Q.op_end;
-            int o = Q.op_begin;
-            uint64_t h = o < end ? P.ops[o].hdr : 0; // headers are read one op ahead
-            if constexpr (INPLACE) {
-                double2 A[R];
+            int o = next_active(sops, Q.op_begin, end, gbase);
+            OpCtx ca, cb;
+            load_ctx(ca, sops[o]);
+            for (;;) {
+                if (o >= end) {
 #pragma unroll
-                for (int i = 0; i < R; ++i) A[i] = buf[wofs + Q.reg_off[i]];
-                for (; o < end; ++o) {
-                    const uint64_t hn = o + 1 < end ? P.ops[o + 1].hdr : 0;
-                    step<RB, true>(A, A, h, P.ops[o], lane, w, gbase);
-                    h = hn;
+                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = a[i];
+                    break;
                 }
+                o = next_active(sops, o + 1, end, gbase);
+                load_ctx(cb, sops[o]);
+                step<RB>(a, b, ca, lane, w, gbase);
+                if (o >= end) {
 #pragma unroll
-                for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = A[i];
-            } else {
-                double2 A[R], B[R];
-#pragma unroll
-                for (int i = 0; i < R; ++i) A[i] = buf[wofs + Q.reg_off[i]];
-                for (; o + 1 < end; o += 2) {
-                    const uint64_t h1 = P.ops[o + 1].hdr;
-                    step<RB, false>(A, B, h, P.ops[o], lane, w, gbase);
-                    h = o + 2 < end ? P.ops[o + 2].hdr : 0;
-                    step<RB, false>(B, A, h1, P.ops[o + 1], lane, w, gbase);
+                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = b[i];
+                    break;
                 }
-                if (o < end) {
-                    step<RB, false>(A, B, h, P.ops[o], lane, w, gbase);
-#pragma unroll
-                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = B[i];
-                } else {
-#pragma unroll
-                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = A[i];
-                }
+                o = next_active(sops, o + 1, end, gbase);
+                load_ctx(ca, sops[o]);
+                step<RB>(b, a, cb, lane, w, gbase);
             }
         }
         fence_proxy_async(); // generic-proxy writes -> visible to the bulk store
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&done[b]);
+        tma_wait_read<0>();  // own part of the store of tile t - 1 has left its stage
+        __syncthreads();
+        copies(t, false);
+        tma_commit();
+        if (t >= 1 && t - 1 + NBUF < ntiles) copies(t - 1 + NBUF, true);
     }
+    tma_wait_all();
 }
 
 } // namespace
 
 void launch_tile_pass(double2* amps, const TileParams& p, cudaStream_t s) {
     constexpr int NBUF = 3;
-#ifndef QGPU_TILE_INPLACE
-#define QGPU_TILE_INPLACE 0
-#endif
-    auto kern = k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF, QGPU_TILE_INPLACE != 0>;
+    auto kern = k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF>;
     constexpr size_t smem = NBUF * (sizeof(double2) << kTileQubits);
     static bool set = false;
     if (!set) {
@@ -484,7 +513,7 @@ void launch_tile_pass(double2* amps, const TileParams& p, cudaStream_t s) {
     }
     uint64_t blocks = p.num_tiles;
     if (blocks > 148) blocks = 148; // persistent: one CTA per SM
-    kern<<<static_cast<unsigned>(blocks), kTileThreads + 32, smem, s>>>(amps, p);
+    kern<<<static_cast<unsigned>(blocks), kTileThreads, smem, s>>>(amps, p);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
         cudaFuncAttributes fa{};
