@@ -24,6 +24,9 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = [
     "-O3", "-std=c++20", "-lineinfo", "--fmad=false",
     "-Xcompiler", "-fPIC,-O3,-ffp-contract=off",
+    # one brx.idx jump table per op switch instead of NVVM's binary
+    # search tree of compares and branches (tile_pass.cu: step)
+    "-Xcicc", "-jump-table-density=1",
     f"-I{INCLUDE}", f"-I{CSRC}",
 ]
 SOURCES = ["kernels.cu", "tile_pass.cu", "runtime.cpp", "api.cpp", "transport.cpp"]

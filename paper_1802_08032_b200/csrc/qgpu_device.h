@@ -82,8 +82,11 @@ struct Mat2 {
 // A CTA owns a tile of 2^kTileQubits amplitudes: the 5 lowest qubits (the
 // lanes: every warp access is 512 contiguous bytes) plus kTileHigh arbitrary
 // higher qubits. The ops of a pass run in phases; in each phase every thread
-// holds 2^kPhaseRegBits amplitudes in registers spanning 4 of the tile's high
-// qubits (the phase's register qubits), the 8 warps span the other 3. Gates
+// holds 2^kPhaseRegBits amplitudes in registers spanning 3 of the tile's high
+// qubits (the phase's register qubits), the 16 warps span the other 4. (8
+// amplitudes x 2 ping-pong copies fit 128 registers, so 4 warps per SM
+// sub-partition hide the op dispatch and FP64 latencies; 16 amplitudes per
+// thread left 2 warps per sub-partition and measured 10 % slower.) Gates
 // on lane qubits use warp shuffles, gates on register qubits stay in
 // registers, diagonal ops and channels act elementwise anywhere; between
 // phases the tile is re-laid out through shared memory. Phase 0 loads from
@@ -92,13 +95,13 @@ struct Mat2 {
 constexpr int kTileQubits = 12;
 constexpr int kTileHigh = kTileQubits - kLaneQubits; // 7
 #ifndef QGPU_PHASE_REG_BITS
-#define QGPU_PHASE_REG_BITS 4
+#define QGPU_PHASE_REG_BITS 3
 #endif
 constexpr int kPhaseRegBits = QGPU_PHASE_REG_BITS;
 constexpr int kTileWarpBits = kTileHigh - kPhaseRegBits; // 3
-constexpr int kTileThreads = 32 << kTileWarpBits;        // 256
+constexpr int kTileThreads = 32 << kTileWarpBits;        // 512 (16 warps)
 constexpr int kMaxPhases = 8;
-constexpr int kMaxTileOps = 64;
+constexpr int kMaxTileOps = 63; // + the stop bit of a phase fits a 64-bit op mask
 
 enum TileLoc : uint8_t { TL_LANE = 0, TL_REG = 1, TL_WARP = 2, TL_OUTER = 3 };
 
@@ -158,6 +161,7 @@ struct TileParams {
     int32_t num_phases;
     int32_t seg_run;                       // high_pos[0..seg_run) = 5, 6, ...: contiguous
     int32_t high_pos[kTileHigh];           // ascending global qubits of tile bits 5..
+    int32_t any_outer;                     // some op has controls outside the tile
     uint64_t seg_off[1 << kTileHigh];      // global offset of tile segment s
     TilePhase phases[kMaxPhases];
     TileOp ops[kMaxTileOps];

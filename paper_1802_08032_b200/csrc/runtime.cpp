@@ -413,6 +413,7 @@ void QuregImpl::launch_tile() {
             }
             to.hdr = tile_hdr(code, flags, op.outcome, q0k, q0p, q1k, q1p, lane_cm, reg_cm, warp_cm);
             to.outer_cmask = outer;
+            if (outer) P.any_outer = 1;
             std::memcpy(to.m, op.m, sizeof(to.m));
         }
     }

@@ -8,9 +8,9 @@
 //    (completion on an mbarrier) and bulk stores at tile boundaries, three
 //    64 KiB stages deep, so the streaming overlaps the ops and no register
 //    holds data in flight;
-//  * the ops run in phases: every consumer thread holds 16 amplitudes in
-//    registers spanning the phase's 4 register qubits (lanes span qubits 0-4,
-//    the 8 consumer warps the remaining 3 tile qubits). Pair ops on register
+//  * the ops run in phases: every thread holds 8 amplitudes in registers
+//    spanning the phase's 3 register qubits (lanes span qubits 0-4, the 16
+//    warps the remaining 4 tile qubits). Pair ops on register
 //    qubits stay in registers, on lane qubits they use warp shuffles, diagonal
 //    gates and channels are elementwise anywhere; between phases the tile is
 //    re-laid out through shared memory.
@@ -19,8 +19,13 @@
 //  * the op table is copied to shared memory once per launch — read from the
 //    kernel-parameter bank every op missed the constant cache;
 //  * an op's header and coefficients are loaded one op ahead (OpCtx), so their
-//    latency hides behind the previous op;
-//  * the host resolves each op to one handler code (TileCode): one jump table;
+//    latency hides behind the previous op; the op index is warp-uniform, so
+//    the loads address through uniform registers;
+//  * the host resolves each op to one handler code (TileCode), and the build
+//    passes -jump-table-density=1 to NVVM: one brx.idx per op instead of a
+//    binary search tree of compares;
+//  * outer-qubit controls are evaluated once per tile (a ballot per 32 ops),
+//    not per op and phase;
 //  * handlers never branch per element on run-time values (selects only where
 //    lane / register controls need them) — per-element branches made ptxas
 //    copy the whole 64-register tile around them;
@@ -256,99 +261,126 @@ struct OpCtx {
     double c[8];
 };
 
-__device__ __forceinline__ void load_ctx(OpCtx& x, const TileOp& op) {
-    x.h = op.hdr;
+// Explicit shared-window addresses: through a generic pointer, ptxas
+// re-derived the CTA's shared window (S2R SR_CgaCtaId) at every op.
+__device__ __forceinline__ void load_ctx(OpCtx& x, uint32_t sops_addr, int o) {
+    const uint32_t a = sops_addr + static_cast<uint32_t>(o) * static_cast<uint32_t>(sizeof(TileOp));
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(x.h) : "r"(a));
 #pragma unroll
-    for (int k = 0; k < 8; ++k) x.c[k] = op.m[k];
+    for (int k = 0; k < 8; k += 2)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                     : "=d"(x.c[k]), "=d"(x.c[k + 1])
+                     : "r"(a + 16u + 8u * static_cast<uint32_t>(k)));
 }
 
-// Controls on outer qubits are uniform per tile: such an op is skipped by the
-// whole CTA (the op loop never visits it). Controls on warp qubits are not
-// skipped but folded into the per-element predicate like lane / register
-// ones: a warp that skipped would idle at the next phase barrier while its
-// sub-partition ran the other warp alone (measured: 32 % barrier stalls).
-__device__ __forceinline__ int next_active(const TileOp* ops, int o, int end, uint64_t gbase) {
-    while (o < end && (gbase & ops[o].outer_cmask) != ops[o].outer_cmask) ++o;
-    return o;
+// Controls on outer qubits are uniform per tile: per tile, each warp
+// evaluates them once for all ops (one ballot per 32 ops) into a 64-bit mask
+// of the ops that run; the op loop walks the set bits. Controls on warp
+// qubits are not skipped but folded into the per-element predicate like lane
+// / register ones: a warp that skipped would idle at the next phase barrier
+// while its sub-partition ran the other warps alone.
+__device__ __forceinline__ uint64_t active_ops(const TileOp* ops, int nops, uint64_t gbase, uint32_t lane) {
+    bool a0 = false, a1 = false;
+    if (static_cast<int>(lane) < nops) {
+        const uint64_t m = ops[lane].outer_cmask;
+        a0 = (gbase & m) == m;
+    }
+    if (static_cast<int>(lane) + 32 < nops) {
+        const uint64_t m = ops[lane + 32].outer_cmask;
+        a1 = (gbase & m) == m;
+    }
+    return static_cast<uint64_t>(__ballot_sync(0xffffffffu, a0)) |
+           static_cast<uint64_t>(__ballot_sync(0xffffffffu, a1)) << 32;
 }
 
-// One op: s -> d.
+__device__ __forceinline__ int lowest(uint64_t m) { return __ffsll(static_cast<long long>(m)) - 1; }
+
+// One op: s -> d. Header fields are decoded inside the arms that use them.
 template <int RB>
 __device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, const OpCtx& x, uint32_t lane,
                                      uint32_t w, uint64_t gbase) {
     const uint64_t h = x.h;
     const uint32_t code = h & 63u;
-    const uint32_t q0p = (h >> 13) & 63u;
-    const uint32_t lane_cm = (h >> 27) & 31u, rcm = (h >> 32) & 15u, warp_cm = (h >> 36) & 15u;
-    const bool tok = (lane & lane_cm) == lane_cm && (w & warp_cm) == warp_cm;
     const double* c = x.c;
+#define QGPU_Q0P ((h >> 13) & 63u)
+#define QGPU_RCM static_cast<uint32_t>((h >> 32) & 15u)
+#define QGPU_TOK                                                                          \
+    ((lane & static_cast<uint32_t>((h >> 27) & 31u)) == static_cast<uint32_t>((h >> 27) & 31u) && \
+     (w & static_cast<uint32_t>((h >> 36) & 15u)) == static_cast<uint32_t>((h >> 36) & 15u))
     switch (code) {
-#define QGPU_REG(CODE, J, CLS, SEL)                                \
-    case CODE: h_reg<RB, J, CLS, SEL>(s, d, c, rcm, tok); break;
-        QGPU_REG(TC_REG + 0, 0, CLS_GENERIC, false)
-        QGPU_REG(TC_REG + 1, 1, CLS_GENERIC, false)
-        QGPU_REG(TC_REG + 2, 2, CLS_GENERIC, false)
-        QGPU_REG(TC_REG + 3, 3, CLS_GENERIC, false)
-        QGPU_REG(TC_REG + 4, 0, CLS_REAL, false)
-        QGPU_REG(TC_REG + 5, 1, CLS_REAL, false)
-        QGPU_REG(TC_REG + 6, 2, CLS_REAL, false)
-        QGPU_REG(TC_REG + 7, 3, CLS_REAL, false)
-        QGPU_REG(TC_REG + 8, 0, CLS_RX, false)
-        QGPU_REG(TC_REG + 9, 1, CLS_RX, false)
-        QGPU_REG(TC_REG + 10, 2, CLS_RX, false)
-        QGPU_REG(TC_REG + 11, 3, CLS_RX, false)
-        QGPU_REG(TC_REG + 12, 0, CLS_SWAP, false)
-        QGPU_REG(TC_REG + 13, 1, CLS_SWAP, false)
-        QGPU_REG(TC_REG + 14, 2, CLS_SWAP, false)
-        QGPU_REG(TC_REG + 15, 3, CLS_SWAP, false)
-        QGPU_REG(TC_REG_SEL + 0, 0, CLS_GENERIC, true)
-        QGPU_REG(TC_REG_SEL + 1, 1, CLS_GENERIC, true)
-        QGPU_REG(TC_REG_SEL + 2, 2, CLS_GENERIC, true)
-        QGPU_REG(TC_REG_SEL + 3, 3, CLS_GENERIC, true)
-        QGPU_REG(TC_REG_SEL + 4, 0, CLS_SWAP, true)
-        QGPU_REG(TC_REG_SEL + 5, 1, CLS_SWAP, true)
-        QGPU_REG(TC_REG_SEL + 6, 2, CLS_SWAP, true)
-        QGPU_REG(TC_REG_SEL + 7, 3, CLS_SWAP, true)
+#define QGPU_REG(CODE, J, CLS)                                     \
+    case CODE: h_reg<RB, J, CLS, false>(s, d, c, 0, true); break;
+        QGPU_REG(TC_REG + 0, 0, CLS_GENERIC)
+        QGPU_REG(TC_REG + 1, 1, CLS_GENERIC)
+        QGPU_REG(TC_REG + 2, 2, CLS_GENERIC)
+        QGPU_REG(TC_REG + 3, 3, CLS_GENERIC)
+        QGPU_REG(TC_REG + 4, 0, CLS_REAL)
+        QGPU_REG(TC_REG + 5, 1, CLS_REAL)
+        QGPU_REG(TC_REG + 6, 2, CLS_REAL)
+        QGPU_REG(TC_REG + 7, 3, CLS_REAL)
+        QGPU_REG(TC_REG + 8, 0, CLS_RX)
+        QGPU_REG(TC_REG + 9, 1, CLS_RX)
+        QGPU_REG(TC_REG + 10, 2, CLS_RX)
+        QGPU_REG(TC_REG + 11, 3, CLS_RX)
+        QGPU_REG(TC_REG + 12, 0, CLS_SWAP)
+        QGPU_REG(TC_REG + 13, 1, CLS_SWAP)
+        QGPU_REG(TC_REG + 14, 2, CLS_SWAP)
+        QGPU_REG(TC_REG + 15, 3, CLS_SWAP)
 #undef QGPU_REG
-    case TC_LANE_GENERIC: h_lane<RB, CLS_GENERIC, false>(s, d, c, q0p, 0, true, lane); break;
-    case TC_LANE_REAL: h_lane<RB, CLS_REAL, false>(s, d, c, q0p, 0, true, lane); break;
-    case TC_LANE_SWAP: h_lane<RB, CLS_SWAP, false>(s, d, c, q0p, 0, true, lane); break;
-    case TC_LANE_SEL_GENERIC: h_lane<RB, CLS_GENERIC, true>(s, d, c, q0p, rcm, tok, lane); break;
-    case TC_LANE_SEL_SWAP: h_lane<RB, CLS_SWAP, true>(s, d, c, q0p, rcm, tok, lane); break;
-#define QGPU_DIAG(CODE, J, DA, SEL)                                \
-    case CODE: h_diag_reg<RB, J, DA, SEL>(s, d, c, rcm, tok); break;
-        QGPU_DIAG(TC_DIAG_REG + 0, 0, true, false)
-        QGPU_DIAG(TC_DIAG_REG + 1, 1, true, false)
-        QGPU_DIAG(TC_DIAG_REG + 2, 2, true, false)
-        QGPU_DIAG(TC_DIAG_REG + 3, 3, true, false)
-        QGPU_DIAG(TC_DIAG_REG_D + 0, 0, false, false)
-        QGPU_DIAG(TC_DIAG_REG_D + 1, 1, false, false)
-        QGPU_DIAG(TC_DIAG_REG_D + 2, 2, false, false)
-        QGPU_DIAG(TC_DIAG_REG_D + 3, 3, false, false)
-        QGPU_DIAG(TC_DIAG_REG_SEL + 0, 0, true, true)
-        QGPU_DIAG(TC_DIAG_REG_SEL + 1, 1, true, true)
-        QGPU_DIAG(TC_DIAG_REG_SEL + 2, 2, true, true)
-        QGPU_DIAG(TC_DIAG_REG_SEL + 3, 3, true, true)
-        QGPU_DIAG(TC_DIAG_REG_D_SEL + 0, 0, false, true)
-        QGPU_DIAG(TC_DIAG_REG_D_SEL + 1, 1, false, true)
-        QGPU_DIAG(TC_DIAG_REG_D_SEL + 2, 2, false, true)
-        QGPU_DIAG(TC_DIAG_REG_D_SEL + 3, 3, false, true)
+#define QGPU_REG_SEL(CODE, J, CLS)                                 \
+    case CODE: h_reg<RB, J, CLS, true>(s, d, c, QGPU_RCM, QGPU_TOK); break;
+        QGPU_REG_SEL(TC_REG_SEL + 0, 0, CLS_GENERIC)
+        QGPU_REG_SEL(TC_REG_SEL + 1, 1, CLS_GENERIC)
+        QGPU_REG_SEL(TC_REG_SEL + 2, 2, CLS_GENERIC)
+        QGPU_REG_SEL(TC_REG_SEL + 3, 3, CLS_GENERIC)
+        QGPU_REG_SEL(TC_REG_SEL + 4, 0, CLS_SWAP)
+        QGPU_REG_SEL(TC_REG_SEL + 5, 1, CLS_SWAP)
+        QGPU_REG_SEL(TC_REG_SEL + 6, 2, CLS_SWAP)
+        QGPU_REG_SEL(TC_REG_SEL + 7, 3, CLS_SWAP)
+#undef QGPU_REG_SEL
+    case TC_LANE_GENERIC: h_lane<RB, CLS_GENERIC, false>(s, d, c, QGPU_Q0P, 0, true, lane); break;
+    case TC_LANE_REAL: h_lane<RB, CLS_REAL, false>(s, d, c, QGPU_Q0P, 0, true, lane); break;
+    case TC_LANE_SWAP: h_lane<RB, CLS_SWAP, false>(s, d, c, QGPU_Q0P, 0, true, lane); break;
+    case TC_LANE_SEL_GENERIC: h_lane<RB, CLS_GENERIC, true>(s, d, c, QGPU_Q0P, QGPU_RCM, QGPU_TOK, lane); break;
+    case TC_LANE_SEL_SWAP: h_lane<RB, CLS_SWAP, true>(s, d, c, QGPU_Q0P, QGPU_RCM, QGPU_TOK, lane); break;
+#define QGPU_DIAG(CODE, J, DA)                                     \
+    case CODE: h_diag_reg<RB, J, DA, false>(s, d, c, 0, true); break;
+        QGPU_DIAG(TC_DIAG_REG + 0, 0, true)
+        QGPU_DIAG(TC_DIAG_REG + 1, 1, true)
+        QGPU_DIAG(TC_DIAG_REG + 2, 2, true)
+        QGPU_DIAG(TC_DIAG_REG + 3, 3, true)
+        QGPU_DIAG(TC_DIAG_REG_D + 0, 0, false)
+        QGPU_DIAG(TC_DIAG_REG_D + 1, 1, false)
+        QGPU_DIAG(TC_DIAG_REG_D + 2, 2, false)
+        QGPU_DIAG(TC_DIAG_REG_D + 3, 3, false)
 #undef QGPU_DIAG
-    case TC_DIAG_LANE: h_diag_lane<RB, false>(s, d, c, (lane >> q0p) & 1u, 0, true); break;
-    case TC_DIAG_LANE_SEL: h_diag_lane<RB, true>(s, d, c, (lane >> q0p) & 1u, rcm, tok); break;
+#define QGPU_DIAG_SEL(CODE, J, DA)                                 \
+    case CODE: h_diag_reg<RB, J, DA, true>(s, d, c, QGPU_RCM, QGPU_TOK); break;
+        QGPU_DIAG_SEL(TC_DIAG_REG_SEL + 0, 0, true)
+        QGPU_DIAG_SEL(TC_DIAG_REG_SEL + 1, 1, true)
+        QGPU_DIAG_SEL(TC_DIAG_REG_SEL + 2, 2, true)
+        QGPU_DIAG_SEL(TC_DIAG_REG_SEL + 3, 3, true)
+        QGPU_DIAG_SEL(TC_DIAG_REG_D_SEL + 0, 0, false)
+        QGPU_DIAG_SEL(TC_DIAG_REG_D_SEL + 1, 1, false)
+        QGPU_DIAG_SEL(TC_DIAG_REG_D_SEL + 2, 2, false)
+        QGPU_DIAG_SEL(TC_DIAG_REG_D_SEL + 3, 3, false)
+#undef QGPU_DIAG_SEL
+    case TC_DIAG_LANE: h_diag_lane<RB, false>(s, d, c, (lane >> QGPU_Q0P) & 1u, 0, true); break;
+    case TC_DIAG_LANE_SEL: h_diag_lane<RB, true>(s, d, c, (lane >> QGPU_Q0P) & 1u, QGPU_RCM, QGPU_TOK); break;
     case TC_DIAG_UNIFORM:
     case TC_DIAG_UNIFORM_SEL: {
         const uint32_t flags = (h >> 6) & 15u;
-        const uint32_t bit = fixed_bit_of((h >> 11) & 3u, q0p, lane, w, gbase);
+        const uint32_t bit = fixed_bit_of((h >> 11) & 3u, QGPU_Q0P, lane, w, gbase);
         if (bit ? (flags & DF_D_ONE) : (flags & DF_A_ONE)) // identity side
             h_copy<RB>(s, d);
         else if (code == TC_DIAG_UNIFORM)
             h_diag_uniform<RB, false>(s, d, c, bit, 0, true);
         else
-            h_diag_uniform<RB, true>(s, d, c, bit, rcm, tok);
+            h_diag_uniform<RB, true>(s, d, c, bit, QGPU_RCM, QGPU_TOK);
         break;
     }
     case TC_DEPHASE: { // density.cpp:56-59: scale where bit(q0) != bit(q1)
+        const uint32_t q0p = QGPU_Q0P;
         const uint32_t q0k = (h >> 11) & 3u, q1k = (h >> 19) & 3u, q1p = (h >> 21) & 63u;
         const uint32_t rm = (q0k == TL_REG ? 1u << q0p : 0u) ^ (q1k == TL_REG ? 1u << q1p : 0u);
         const uint32_t f = (q0k == TL_REG ? 0u : fixed_bit_of(q0k, q0p, lane, w, gbase)) ^
@@ -363,6 +395,7 @@ __device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, const OpCtx
         break;
     }
     case TC_COLLAPSE: { // keep bit(q0) (and bit(q1)) == outcome, scaled
+        const uint32_t q0p = QGPU_Q0P;
         const uint32_t flags = (h >> 6) & 15u;
         const uint32_t q0k = (h >> 11) & 3u, q1k = (h >> 19) & 3u, q1p = (h >> 21) & 63u;
         const uint32_t o = (h >> 10) & 1u;
@@ -382,10 +415,16 @@ __device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, const OpCtx
     }
     default: __builtin_unreachable(); // the host emits TileCode values only
     }
+#undef QGPU_Q0P
+#undef QGPU_RCM
+#undef QGPU_TOK
 }
 
+// Global index of tile T's amplitude 0: T's bits deposited into the qubits
+// outside the tile. Linear in T, so a table per byte of T (built once per
+// launch) replaces the per-bit insertion loop.
 template <int RB, int WB>
-__device__ __forceinline__ uint64_t tile_gbase(const TileParams& P, uint64_t T) {
+__device__ __forceinline__ uint64_t tile_gbase_slow(const TileParams& P, uint64_t T) {
     uint64_t gb = T << kLaneQubits;
 #pragma unroll
     for (int j = 0; j < RB + WB; ++j) gb = insert_zero_bit(gb, P.high_pos[j]);
@@ -415,8 +454,18 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
     const uint32_t lane = threadIdx.x & 31u;
     const uint32_t w = threadIdx.x >> 5;
     const int nph = P.num_phases;
+    const bool any_outer = P.any_outer != 0;
+    constexpr int kGbaseChunks = 3; // tile indices < 2^24 (<= 36 local qubits)
     const uint64_t G = gridDim.x;
     const uint64_t ntiles = P.num_tiles > blockIdx.x ? (P.num_tiles - blockIdx.x + G - 1) / G : 0;
+
+    __shared__ uint64_t gtab[kGbaseChunks][256];
+    auto tile_gbase = [&](uint64_t T) {
+        uint64_t g = 0;
+#pragma unroll
+        for (int k = 0; k < kGbaseChunks; ++k) g |= gtab[k][(T >> (8 * k)) & 255u];
+        return g;
+    };
 
     // runs of 2^seg_run segments are contiguous in HBM: one bulk copy each,
     // spread over the threads. The expected byte count may be posted after
@@ -425,7 +474,7 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
     const int run = P.seg_run;
     auto copies = [&](uint64_t t, bool load) {
         const int b = static_cast<int>(t % NBUF);
-        const uint64_t gb = tile_gbase<RB, WB>(P, blockIdx.x + t * G);
+        const uint64_t gb = tile_gbase(blockIdx.x + t * G);
         double2* buf = smem + (static_cast<size_t>(b) << K);
         if (load && threadIdx.x == 0) mbar_expect_tx(&full[b], TILE_BYTES);
         for (int sg = static_cast<int>(threadIdx.x) << run; sg < NSEG; sg += blockDim.x << run) {
@@ -442,52 +491,67 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
         for (int b = 0; b < NBUF; ++b) mbar_init(&full[b], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
+    for (int k = threadIdx.x; k < kGbaseChunks * 256; k += blockDim.x)
+        gtab[k >> 8][k & 255] = tile_gbase_slow<RB, WB>(P, static_cast<uint64_t>(k & 255) << (8 * (k >> 8)));
     __syncthreads();
     for (uint64_t t = 0; t < NBUF && t < ntiles; ++t) copies(t, true);
+    const int nops = P.phases[nph - 1].op_end;
+    const uint32_t sops_addr = smem_u32(sops);
     {
-        const int nops = P.phases[nph - 1].op_end;
         const uint64_t* src = reinterpret_cast<const uint64_t*>(P.ops);
         uint64_t* dst = reinterpret_cast<uint64_t*>(sops);
         constexpr int WORDS = sizeof(TileOp) / sizeof(uint64_t);
-        for (int k = threadIdx.x; k < nops * WORDS; k += blockDim.x) dst[k] = src[k];
+        for (int k = threadIdx.x; k < (kMaxTileOps + 1) * WORDS; k += blockDim.x)
+            dst[k] = k < nops * WORDS ? src[k] : 0; // entry kMaxTileOps: the prefetch sentinel
     }
     __syncthreads();
 
     for (uint64_t t = 0; t < ntiles; ++t) {
         const int b = static_cast<int>(t % NBUF);
         double2* buf = smem + (static_cast<size_t>(b) << K);
-        const uint64_t gbase = tile_gbase<RB, WB>(P, blockIdx.x + t * G) + P.global_offset;
+        const uint64_t gbase = tile_gbase(blockIdx.x + t * G) + P.global_offset;
+        const uint64_t act = any_outer ? active_ops(sops, nops, gbase, lane) : ~uint64_t{0};
         mbar_wait(&full[b], static_cast<uint32_t>((t / NBUF) & 1));
         for (int ph = 0; ph < nph; ++ph) {
-            if (ph > 0) __syncthreads(); // previous phase's writes are in
             const TilePhase& Q = P.phases[ph];
+            const int end = Q.op_end;
+            uint64_t m = act & ((uint64_t{1} << end) - 1) &
+                         ~((uint64_t{1} << Q.op_begin) - 1);
+            if (m == 0) continue; // no op runs: the tile stays as it is in shared memory
+            // end < 64 always: kMaxTileOps entries plus the sentinel
+            if (ph > 0) __syncthreads(); // previous phase's writes are in
             const uint32_t wofs = Q.warp_off[w] + lane;
             double2 a[R], b[R];
 #pragma unroll
             for (int i = 0; i < R; ++i) a[i] = buf[wofs + Q.reg_off[i]];
             // ops alternate a -> b, b -> a; the contexts alternate too, each
-            // loaded one op ahead (sops has a spare entry past the last op)
-            const int end = Q.op_end;
-            int o = next_active(sops, Q.op_begin, end, gbase);
+            // loaded one op ahead. `run` has a bit per op that runs on this
+            // tile, plus a stop bit at the phase end (sops[end] is a valid
+            // entry: the next phase's first op or the zero sentinel).
+            const uint64_t runm = m | (uint64_t{1} << end);
+            int o = Q.op_begin;
+            while (!((runm >> o) & 1u)) ++o;
             OpCtx ca, cb;
-            load_ctx(ca, sops[o]);
+            load_ctx(ca, sops_addr, o);
             for (;;) {
+                int on = o + 1;
+                while (!((runm >> on) & 1u)) ++on;
+                load_ctx(cb, sops_addr, on);
+                step<RB>(a, b, ca, lane, w, gbase);
+                if (on >= end) {
+#pragma unroll
+                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = b[i];
+                    break;
+                }
+                o = on + 1;
+                while (!((runm >> o) & 1u)) ++o;
+                load_ctx(ca, sops_addr, o);
+                step<RB>(b, a, cb, lane, w, gbase);
                 if (o >= end) {
 #pragma unroll
                     for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = a[i];
                     break;
                 }
-                o = next_active(sops, o + 1, end, gbase);
-                load_ctx(cb, sops[o]);
-                step<RB>(a, b, ca, lane, w, gbase);
-                if (o >= end) {
-#pragma unroll
-                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = b[i];
-                    break;
-                }
-                o = next_active(sops, o + 1, end, gbase);
-                load_ctx(ca, sops[o]);
-                step<RB>(b, a, cb, lane, w, gbase);
             }
         }
         fence_proxy_async(); // generic-proxy writes -> visible to the bulk store
