@@ -92,14 +92,21 @@ struct Mat2 {
 // phases the tile is re-laid out through shared memory. Phase 0 loads from
 // HBM and the last phase stores to HBM, so a pass is one read + one write of
 // the state whatever its op count.
-constexpr int kTileQubits = 12;
-constexpr int kTileHigh = kTileQubits - kLaneQubits; // 7
 #ifndef QGPU_PHASE_REG_BITS
 #define QGPU_PHASE_REG_BITS 3
 #endif
+#ifndef QGPU_TILE_GROUP_BITS
+#define QGPU_TILE_GROUP_BITS 0
+#endif
+#ifndef QGPU_TILE_WARP_BITS
+#define QGPU_TILE_WARP_BITS (4 - QGPU_TILE_GROUP_BITS)
+#endif
 constexpr int kPhaseRegBits = QGPU_PHASE_REG_BITS;
-constexpr int kTileWarpBits = kTileHigh - kPhaseRegBits; // 3
-constexpr int kTileThreads = 32 << kTileWarpBits;        // 512 (16 warps)
+constexpr int kTileWarpBits = QGPU_TILE_WARP_BITS;  // warps per tile group: 2^WB
+constexpr int kTileGroupBits = QGPU_TILE_GROUP_BITS; // independent tile groups per CTA
+constexpr int kTileQubits = kLaneQubits + kPhaseRegBits + kTileWarpBits;
+constexpr int kTileHigh = kTileQubits - kLaneQubits;
+constexpr int kTileThreads = 32 << (kTileWarpBits + kTileGroupBits); // 512 (16 warps)
 constexpr int kMaxPhases = 8;
 constexpr int kMaxTileOps = 63; // + the stop bit of a phase fits a 64-bit op mask
 
@@ -149,9 +156,16 @@ constexpr uint64_t tile_hdr(uint32_t code, uint32_t flags, uint32_t outcome,
            uint64_t(reg_cm & 15) << 32 | uint64_t(warp_cm & 15) << 36;
 }
 
+// Lane bits 0-2 always span qubits 0-2 (a quarter-warp's 8 lanes read 128
+// contiguous bytes: conflict-free LDS/STS.128 on the linear tile); lane bits
+// 3 and 4 may carry any tile qubit per phase, so qubits 3 and 4 can be
+// register qubits like the high ones.
+constexpr int kFixedLaneBits = 3;
+
 struct TilePhase {
     uint16_t reg_off[1 << kPhaseRegBits];  // tile index of register i (lane 0, warp 0)
     uint16_t warp_off[1 << kTileWarpBits]; // tile index offset of warp w
+    uint16_t lane_off[2];                  // tile index offsets of lane bits 3, 4
     uint16_t op_begin, op_end;
 };
 

@@ -209,21 +209,27 @@ bool QuregImpl::use_tile() const { return local_qubits >= kTileQubits; }
 
 bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
     if (phases.empty()) phases.push_back(PhaseState{});
-    if (pair && op.q0 >= kLaneQubits) {
+    if (pair && op.q0 >= kFixedLaneBits) {
         const int q = op.q0;
-        const bool in_tile = std::find(tile_high.begin(), tile_high.end(), q) != tile_high.end();
-        if (!in_tile && static_cast<int>(tile_high.size()) >= kTileHigh) return false;
-        // a phase holds kPhaseRegBits register qubits
         PhaseState& ph = phases.back();
         const bool in_phase = std::find(ph.regs.begin(), ph.regs.end(), q) != ph.regs.end();
-        if (!in_phase && static_cast<int>(ph.regs.size()) >= kPhaseRegBits) {
-            if (static_cast<int>(phases.size()) >= kMaxPhases) return false;
-            PhaseState next;
-            next.op_begin = static_cast<int>(pending.size());
-            phases.push_back(next);
+        if (q < kLaneQubits) {
+            // qubits 3, 4: a register qubit if the phase has room, else a
+            // lane qubit of this phase (a shuffle op; a new phase costs more)
+            if (!in_phase && static_cast<int>(ph.regs.size()) < kPhaseRegBits) ph.regs.push_back(q);
+        } else {
+            const bool in_tile = std::find(tile_high.begin(), tile_high.end(), q) != tile_high.end();
+            if (!in_tile && static_cast<int>(tile_high.size()) >= kTileHigh) return false;
+            // a phase holds kPhaseRegBits register qubits
+            if (!in_phase && static_cast<int>(ph.regs.size()) >= kPhaseRegBits) {
+                if (static_cast<int>(phases.size()) >= kMaxPhases) return false;
+                PhaseState next;
+                next.op_begin = static_cast<int>(pending.size());
+                phases.push_back(next);
+            }
+            if (!in_phase) phases.back().regs.push_back(q);
+            if (!in_tile) tile_high.push_back(q);
         }
-        if (!in_phase) phases.back().regs.push_back(q);
-        if (!in_tile) tile_high.push_back(q);
     }
     pending.push_back(op);
     return true;
@@ -307,13 +313,19 @@ void QuregImpl::launch_tile() {
     }
     for (size_t p = 0; p < phases.size(); ++p) {
         TilePhase& Q = P.phases[p];
-        // register bits: the phase's targets, then other tile bits
-        std::vector<int> rb, wb;
+        // register bits: the phase's targets, then other tile bits; lane bits
+        // 3, 4: qubits 3, 4 unless they are registers, else the lowest free
+        // high bits; warp bits: the rest
+        std::vector<int> rb, lb, wb;
         for (int q : phases[p].regs) rb.push_back(tbit(q));
         for (int t = kLaneQubits; t < kTileQubits && static_cast<int>(rb.size()) < kPhaseRegBits; ++t)
             if (std::find(rb.begin(), rb.end(), t) == rb.end()) rb.push_back(t);
-        for (int t = kLaneQubits; t < kTileQubits; ++t)
-            if (std::find(rb.begin(), rb.end(), t) == rb.end()) wb.push_back(t);
+        for (int t = kFixedLaneBits; t < kTileQubits && lb.size() < 2; ++t)
+            if (std::find(rb.begin(), rb.end(), t) == rb.end()) lb.push_back(t);
+        for (int t = kFixedLaneBits; t < kTileQubits; ++t)
+            if (std::find(rb.begin(), rb.end(), t) == rb.end() &&
+                std::find(lb.begin(), lb.end(), t) == lb.end())
+                wb.push_back(t);
         for (int i = 0; i < (1 << kPhaseRegBits); ++i) {
             uint32_t off = 0;
             for (int j = 0; j < kPhaseRegBits; ++j)
@@ -326,6 +338,7 @@ void QuregImpl::launch_tile() {
                 if ((w >> j) & 1) off |= 1u << wb[j];
             Q.warp_off[w] = static_cast<uint16_t>(off);
         }
+        for (int j = 0; j < 2; ++j) Q.lane_off[j] = static_cast<uint16_t>(1u << lb[j]);
         const int begin = phases[p].op_begin;
         const int end = p + 1 < phases.size() ? phases[p + 1].op_begin : static_cast<int>(pending.size());
         Q.op_begin = static_cast<uint16_t>(begin);
@@ -338,10 +351,16 @@ void QuregImpl::launch_tile() {
             } else if (t < 0) {
                 *kind = TL_OUTER;
                 *pos = static_cast<uint8_t>(q);
-            } else if (t < kLaneQubits) {
+            } else if (t < kFixedLaneBits) {
                 *kind = TL_LANE;
                 *pos = static_cast<uint8_t>(t);
             } else {
+                for (int j = 0; j < 2; ++j)
+                    if (lb[j] == t) {
+                        *kind = TL_LANE;
+                        *pos = static_cast<uint8_t>(kFixedLaneBits + j);
+                        return;
+                    }
                 for (int j = 0; j < kPhaseRegBits; ++j)
                     if (rb[j] == t) {
                         *kind = TL_REG;

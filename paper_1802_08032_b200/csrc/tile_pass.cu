@@ -455,7 +455,7 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
     const uint32_t w = threadIdx.x >> 5;
     const int nph = P.num_phases;
     const bool any_outer = P.any_outer != 0;
-    constexpr int kGbaseChunks = 3; // tile indices < 2^24 (<= 36 local qubits)
+    constexpr int kGbaseChunks = (36 - K + 7) / 8; // tile indices of <= 36 local qubits
     const uint64_t G = gridDim.x;
     const uint64_t ntiles = P.num_tiles > blockIdx.x ? (P.num_tiles - blockIdx.x + G - 1) / G : 0;
 
@@ -520,7 +520,8 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
             if (m == 0) continue; // no op runs: the tile stays as it is in shared memory
             // end < 64 always: kMaxTileOps entries plus the sentinel
             if (ph > 0) __syncthreads(); // previous phase's writes are in
-            const uint32_t wofs = Q.warp_off[w] + lane;
+            const uint32_t wofs = Q.warp_off[w] + (lane & 7u) + ((lane >> 3) & 1u ? Q.lane_off[0] : 0u) +
+                                  ((lane >> 4) & 1u ? Q.lane_off[1] : 0u);
             double2 a[R], b[R];
 #pragma unroll
             for (int i = 0; i < R; ++i) a[i] = buf[wofs + Q.reg_off[i]];
