@@ -13,7 +13,9 @@
 #include "runtime.h"
 #include "transport.h"
 
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <ctime>
@@ -284,6 +286,10 @@ QuESTEnv make_env(Mode mode, int rank, int nranks, int device, const char* id128
     const uint64_t seeds[2] = {static_cast<uint64_t>(std::time(nullptr)),
                                static_cast<uint64_t>(getpid())};
     e->rng = fold_seeds(seeds, 2);
+    if (const char* v = std::getenv("QGPU_TILE_TARGETS"))
+        e->tile_targets = std::clamp(std::atoi(v), 1, qgpu::kTileHigh);
+    if (const char* v = std::getenv("QGPU_TILE_PHASES"))
+        e->tile_phases = std::clamp(std::atoi(v), 1, qgpu::kMaxPhases);
     if (mode == Mode::Nccl && nranks > 1) e->nccl = std::make_unique<NcclComm>(rank, nranks, id128);
     QuESTEnv out;
     out.rank = mode == Mode::Loopback ? 0 : rank;

@@ -219,10 +219,10 @@ bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
             if (!in_phase && static_cast<int>(ph.regs.size()) < kPhaseRegBits) ph.regs.push_back(q);
         } else {
             const bool in_tile = std::find(tile_high.begin(), tile_high.end(), q) != tile_high.end();
-            if (!in_tile && static_cast<int>(tile_high.size()) >= kTileHigh) return false;
+            if (!in_tile && static_cast<int>(tile_high.size()) >= env->tile_targets) return false;
             // a phase holds kPhaseRegBits register qubits
             if (!in_phase && static_cast<int>(ph.regs.size()) >= kPhaseRegBits) {
-                if (static_cast<int>(phases.size()) >= kMaxPhases) return false;
+                if (static_cast<int>(phases.size()) >= env->tile_phases) return false;
                 PhaseState next;
                 next.op_begin = static_cast<int>(pending.size());
                 phases.push_back(next);

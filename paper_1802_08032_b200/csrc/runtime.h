@@ -45,6 +45,16 @@ struct Env {
     int fusion_mode = 0; // 0 fused, 1 one pass per op, 2 simple per-op kernels
     int max_ops = kMaxPassOps;
     int reg_qubits = 4;
+    // tile-pass shape limits (scheduler tuning; QGPU_TILE_TARGETS /
+    // QGPU_TILE_PHASES override them at Env creation). A phase transition
+    // (a shared-memory round trip of the whole tile plus a block barrier)
+    // costs about three register ops, and a fresh pass is free while the pass
+    // stays HBM-bound: measured on the 30-qubit layered circuit, at most two
+    // phases per pass is fastest (profiles/r1_scheduler_knobs.md), and a
+    // dynamic-programming pass planner over a calibrated cost model predicted
+    // no further gain.
+    int tile_targets = kTileHigh; // distinct pair targets above qubit 4 per pass
+    int tile_phases = 2;          // register phases per pass
     uint64_t chunk_amps = uint64_t{1} << 24;
     std::unique_ptr<NcclComm> nccl;
     std::set<struct QuregImpl*> quregs;

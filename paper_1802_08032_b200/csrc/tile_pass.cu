@@ -530,13 +530,13 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
             // tile, plus a stop bit at the phase end (sops[end] is a valid
             // entry: the next phase's first op or the zero sentinel).
             const uint64_t runm = m | (uint64_t{1} << end);
-            int o = Q.op_begin;
-            while (!((runm >> o) & 1u)) ++o;
+            // next op at or after `from`: one bit scan (runm has the stop bit)
+            auto next = [&](int from) { return lowest(runm & (~uint64_t{0} << from)); };
+            int o = next(Q.op_begin);
             OpCtx ca, cb;
             load_ctx(ca, sops_addr, o);
             for (;;) {
-                int on = o + 1;
-                while (!((runm >> on) & 1u)) ++on;
+                const int on = next(o + 1);
                 load_ctx(cb, sops_addr, on);
                 step<RB>(a, b, ca, lane, w, gbase);
                 if (on >= end) {
@@ -544,8 +544,7 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
                     for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = b[i];
                     break;
                 }
-                o = on + 1;
-                while (!((runm >> o) & 1u)) ++o;
+                o = next(on + 1);
                 load_ctx(ca, sops_addr, o);
                 step<RB>(b, a, cb, lane, w, gbase);
                 if (o >= end) {

@@ -17,17 +17,19 @@ p.add_argument("--qubits", type=int, default=30)
 p.add_argument("--kinds", default="RZ,RY,RX,H,X")
 p.add_argument("--counts", default="1,4,8,16,32")
 p.add_argument("--targets", default="5,6,7,8,9,10,11")
+p.add_argument("--controls", default="")
 p.add_argument("--reps", type=int, default=3)
 a = p.parse_args()
 tg = [int(x) for x in a.targets.split(",")]
+ct = tuple(int(x) for x in a.controls.split(",")) if a.controls else ()
 env = quest.Env()
 q = quest.QuregHandle(env, a.qubits)
 ab = 2 * 16 * 2.0 ** a.qubits
 for kind in a.kinds.split(","):
     row = []
     for n in [int(x) for x in a.counts.split(",")]:
-        ops = [C.GateOp(kind, tg[k % len(tg)], angle=0.1 + 0.01 * k) if kind in C.HAS_ANGLE
-               else C.GateOp(kind, tg[k % len(tg)]) for k in range(n)]
+        ops = [C.GateOp(kind, tg[k % len(tg)], controls=ct, angle=0.1 + 0.01 * k) if kind in C.HAS_ANGLE
+               else C.GateOp(kind, tg[k % len(tg)], controls=ct) for k in range(n)]
         c = C.Circuit(a.qubits, 0, ops)
         C.apply_circuit(q, c)
         q.flush()
