@@ -102,6 +102,26 @@ int qgpuPlanGate(int flatQubits, int rankLog2, int rank, int target,
 int qgpuPlanChunks(unsigned long long localLen, unsigned long long chunkAmps,
                    unsigned long long* chunkLen);
 
+/* Memory plan. The reference's node model, restated:
+ * modeled peak bytes per rank of an n-qubit vector on 2^rankLog2 ranks for
+ * strategy 0 = FullClone (2x), 1 = HalfExchange (1.5x), 2 = PerAmplitude
+ * (1x + blockAmps), double or single precision
+ * (qsim::modeled_bytes_per_rank, distributed.cpp:436-446; returns 0, or -1
+ * on invalid input / 64-bit overflow), and the largest n that fits
+ * nodeBytes - overheadBytes (qsim::max_qubits, distributed.cpp:448-468). */
+int qgpuModeledBytesPerRank(int numQubits, int rankLog2, int strategy, int singlePrecision,
+                            unsigned long long blockAmps, unsigned long long* bytes);
+int qgpuMaxQubits(unsigned long long nodeBytes, unsigned long long overheadBytes, int strategy,
+                  int singlePrecision, int rankLog2);
+/* This runtime's device footprint per rank: the partition (16 B x
+ * 2^(flat - k)), two exchange sub-chunk buffers of chunkAmps amplitudes once
+ * k > 0, and the reduction scratch; and the largest register (qubits, or N
+ * of an N-qubit density matrix) whose footprint fits deviceBytes.
+ * createQureg preflights against free HBM with the same numbers. */
+unsigned long long qgpuDeviceBytesPerRank(int flatQubits, int rankLog2, unsigned long long chunkAmps);
+int qgpuDeviceMaxQubits(unsigned long long deviceBytes, int rankLog2, unsigned long long chunkAmps,
+                        int density);
+
 #ifdef __cplusplus
 }
 #endif

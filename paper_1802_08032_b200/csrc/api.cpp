@@ -1013,4 +1013,36 @@ int qgpuPlanChunks(unsigned long long localLen, unsigned long long chunkAmps,
     return static_cast<int>((localLen + c - 1) / c);
 }
 
+// ------------------------------------------------------------ memory plan
+
+int qgpuModeledBytesPerRank(int numQubits, int rankLog2, int strategy, int singlePrecision,
+                            unsigned long long blockAmps, unsigned long long* bytes) {
+    return guarded("qgpuModeledBytesPerRank", -1, [&] {
+        const uint64_t b = qgpu::modeled_bytes_per_rank(numQubits, rankLog2, strategy,
+                                                        singlePrecision != 0, blockAmps);
+        if (bytes) *bytes = b;
+        return 0;
+    });
+}
+
+int qgpuMaxQubits(unsigned long long nodeBytes, unsigned long long overheadBytes, int strategy,
+                  int singlePrecision, int rankLog2) {
+    return guarded("qgpuMaxQubits", -1, [&] {
+        return qgpu::max_qubits(nodeBytes, overheadBytes, strategy, singlePrecision != 0, rankLog2);
+    });
+}
+
+unsigned long long qgpuDeviceBytesPerRank(int flatQubits, int rankLog2, unsigned long long chunkAmps) {
+    return guarded("qgpuDeviceBytesPerRank", 0ull, [&] {
+        return static_cast<unsigned long long>(qgpu::device_bytes_per_rank(flatQubits, rankLog2, chunkAmps));
+    });
+}
+
+int qgpuDeviceMaxQubits(unsigned long long deviceBytes, int rankLog2, unsigned long long chunkAmps,
+                        int density) {
+    return guarded("qgpuDeviceMaxQubits", -1, [&] {
+        return qgpu::device_max_qubits(deviceBytes, rankLog2, chunkAmps, density != 0);
+    });
+}
+
 } // extern "C"

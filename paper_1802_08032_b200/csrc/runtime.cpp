@@ -119,6 +119,26 @@ QuregImpl* create_register(Env* env, int N, bool density) {
         throw DomainError("density matrix of " + std::to_string(N) +
                           " qubits cannot be split over 2^" + std::to_string(env->rank_log2) +
                           " ranks (need k <= N)");
+    // preflight against free HBM (an infeasible size is a
+    // resource error citing max_qubits)
+    {
+        size_t free_b = 0, total_b = 0;
+        if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+            const int nsh = env->mode == Mode::Loopback ? env->num_ranks : 1;
+            const uint64_t per = device_bytes_per_rank(flat, env->rank_log2, env->chunk_amps);
+            const unsigned __int128 need = static_cast<unsigned __int128>(per) * nsh;
+            if (need > free_b) {
+                const int mq = device_max_qubits(free_b / nsh, env->rank_log2, env->chunk_amps, density);
+                throw ResourceError("register of " + std::to_string(N) + " qubits needs " +
+                                    std::to_string(per) + " bytes per rank but " +
+                                    std::to_string(free_b) + " bytes of device memory are free: " +
+                                    "max_qubits = " + std::to_string(mq) + " at 2^" +
+                                    std::to_string(env->rank_log2) + " ranks");
+            }
+        } else {
+            cudaGetLastError();
+        }
+    }
     auto q = std::make_unique<QuregImpl>();
     q->env = env;
     q->N = N;

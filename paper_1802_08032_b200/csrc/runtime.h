@@ -172,6 +172,13 @@ struct QuregImpl {
 QuregImpl* create_register(Env* env, int N, bool density);
 
 // Pure planner (qgpu.h: qgpuPlanGate).
+// memory_plan.cpp: the reference's node model (distributed.cpp:423-468) and
+// this runtime's per-rank device footprint
+uint64_t modeled_bytes_per_rank(int n, int k, int strategy, bool single, uint64_t block);
+int max_qubits(uint64_t node_bytes, uint64_t overhead, int strategy, bool single, int k);
+uint64_t device_bytes_per_rank(int flat, int k, uint64_t chunk_amps);
+int device_max_qubits(uint64_t device_bytes, int k, uint64_t chunk_amps, bool density);
+
 int plan_gate(int flat, int rank_log2, int rank, int target, uint64_t cmask, int* peer,
               int* own_lo, uint64_t* low_mask);
 

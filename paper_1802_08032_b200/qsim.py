@@ -338,3 +338,28 @@ def pair_rank(plan: PartitionPlan, rank: int, target: int) -> int:
         raise DomainError(f"gate on qubit {target} is rank-local; no pair rank exists")
     kind, peer, _, _ = quest.plan_gate(plan.num_qubits, plan.rank_count_log2, rank, target, 0)
     return peer
+
+
+# ------------------------------------------------------------ memory model
+
+@dataclass
+class MemoryModel:
+    """distributed.hpp:145-150 (node budget for a strategy / precision)."""
+
+    node_bytes: int = 0
+    overhead_bytes: int = 50 << 20
+    strategy: str = "full_clone"
+    precision: str = "double"
+
+
+def modeled_bytes_per_rank(num_qubits: int, rank_count_log2: int, strategy: str = "full_clone",
+                           precision: str = "double", block_amps: int = 1) -> int:
+    """distributed.cpp:436-446 over qgpuModeledBytesPerRank."""
+    return quest.modeled_bytes_per_rank(num_qubits, rank_count_log2, strategy, precision == "single",
+                                        block_amps)
+
+
+def max_qubits(model: MemoryModel, rank_count_log2: int) -> int:
+    """distributed.cpp:448-468 over qgpuMaxQubits."""
+    return quest.max_qubits(model.node_bytes, rank_count_log2, model.strategy,
+                            model.precision == "single", model.overhead_bytes)

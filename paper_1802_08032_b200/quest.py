@@ -157,6 +157,10 @@ _SIGS = {
     "qgpuCommStats": (None, [Qureg, _VP, _VP]),
     "qgpuPlanGate": (_I, [_I, _I, _I, _I, _ULL, _IP, _IP, ctypes.POINTER(ctypes.c_ulonglong)]),
     "qgpuPlanChunks": (_I, [_ULL, _ULL, ctypes.POINTER(ctypes.c_ulonglong)]),
+    "qgpuModeledBytesPerRank": (_I, [_I, _I, _I, _I, _ULL, ctypes.POINTER(ctypes.c_ulonglong)]),
+    "qgpuMaxQubits": (_I, [_ULL, _ULL, _I, _I, _I]),
+    "qgpuDeviceBytesPerRank": (_ULL, [_I, _I, _ULL]),
+    "qgpuDeviceMaxQubits": (_I, [_ULL, _I, _ULL, _I]),
     "qgpuProfileStart": (None, [QuESTEnv]),
     "qgpuProfileStop": (_I, [QuESTEnv, _VP, _VP, _I]),
 }
@@ -373,3 +377,39 @@ def plan_chunks(local_len: int, chunk: int):
     c = ctypes.c_ulonglong()
     n = lib().qgpuPlanChunks(local_len, chunk, ctypes.byref(c))
     return n, c.value
+
+
+STRATEGIES = {"full_clone": 0, "half_exchange": 1, "per_amplitude": 2}
+
+
+def modeled_bytes_per_rank(n: int, k: int, strategy: str = "full_clone", single: bool = False,
+                           block_amps: int = 1) -> int:
+    """qgpuModeledBytesPerRank (the reference's node model)."""
+    out = ctypes.c_ulonglong()
+    r = lib().qgpuModeledBytesPerRank(n, k, STRATEGIES[strategy], int(single), block_amps, ctypes.byref(out))
+    if r < 0:
+        check()
+    return out.value
+
+
+def max_qubits(node_bytes: int, k: int, strategy: str = "full_clone", single: bool = False,
+               overhead: int = 50 << 20) -> int:
+    """qgpuMaxQubits (the reference's max_qubits)."""
+    r = lib().qgpuMaxQubits(node_bytes, overhead, STRATEGIES[strategy], int(single), k)
+    if r < 0:
+        check()
+    return r
+
+
+def device_bytes_per_rank(flat: int, k: int, chunk_amps: int = 1 << 24) -> int:
+    r = lib().qgpuDeviceBytesPerRank(flat, k, chunk_amps)
+    if r == 0:
+        check()
+    return r
+
+
+def device_max_qubits(device_bytes: int, k: int, chunk_amps: int = 1 << 24, density: bool = False) -> int:
+    r = lib().qgpuDeviceMaxQubits(device_bytes, k, chunk_amps, int(density))
+    if r < 0:
+        check()
+    return r
