@@ -82,6 +82,23 @@ int qgpuGetNcclUniqueId(char* out128);
 QuESTEnv qgpuCreateNcclEnv(int rank, int numRanks, int device, const char* uniqueId128);
 /* Exchange sub-chunk size in amplitudes (power of two, default 2^24). */
 void qgpuSetExchangeChunk(QuESTEnv env, long long int amps);
+/* Global<->local qubit swaps (default on): a gate whose target is a global
+ * (rank-bit) qubit first swaps that qubit with the least recently used local
+ * one — each rank trades half its partition with its partner once — instead
+ * of exchanging the whole partition for every such gate as the reference
+ * does (distributed.cpp:167-231). Amplitudes are bit-identical either way;
+ * 0 selects the reference's per-gate exchange. Registers of this env are
+ * first returned to the identity qubit layout. */
+void qgpuSetQubitSwaps(QuESTEnv env, int enable);
+
+/* The swap planner alone (host only, no GPU): for numOps ops on logical
+ * flat qubits targets[k] (pairOps[k] != 0 for a 2x2 non-diagonal gate,
+ * 0 for a diagonal op) on 2^rankLog2 ranks, the swaps the runtime performs:
+ * swapsOut[3i..3i+2] = (op index, global position, local position).
+ * Returns the number of swaps, or -1 on invalid input. */
+int qgpuPlanSwaps(int flatQubits, int rankLog2, unsigned long long chunkAmps, int numOps,
+                  const int* targets, const int* pairOps, int* swapsOut, int maxSwaps);
+
 /* Messages / bytes this process's ranks sent for `qureg` (CommStats,
  * distributed.hpp:63-74); arrays of length numRanks (loopback) or 1. */
 void qgpuCommStats(Qureg qureg, unsigned long long* messages, unsigned long long* bytes);

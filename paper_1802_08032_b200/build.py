@@ -29,7 +29,7 @@ COMMON = [
     "-Xcicc", "-jump-table-density=1",
     f"-I{INCLUDE}", f"-I{CSRC}",
 ]
-SOURCES = ["kernels.cu", "tile_pass.cu", "runtime.cpp", "api.cpp", "transport.cpp", "memory_plan.cpp"]
+SOURCES = ["kernels.cu", "tile_pass.cu", "runtime.cpp", "api.cpp", "transport.cpp", "memory_plan.cpp", "swap_plan.cpp"]
 
 
 def _headers() -> list[Path]:

@@ -521,6 +521,7 @@ Qureg createCloneQureg(Qureg qureg, QuESTEnv env) {
         QuregImpl* src = reg_of(qureg);
         QuregImpl* r = create_register(env_of(env), src->N, src->density);
         src->flush();
+        r->sp = src->sp; // same logical -> physical qubit map
         for (size_t k = 0; k < r->shards.size(); ++k)
             cuda_check(cudaMemcpyAsync(r->shards[k].amps, src->shards[k].amps,
                                        r->local_len * sizeof(double2), cudaMemcpyDeviceToDevice,
@@ -676,7 +677,8 @@ void cloneQureg(Qureg targetQureg, Qureg copyQureg) {
         if (t->density != c->density || t->N != c->N || t->env != c->env)
             throw qgpu::DomainError("cloneQureg needs registers of the same kind and size");
         c->flush();
-        t->discard();
+        t->discard_all();
+        t->sp = c->sp;
         for (size_t k = 0; k < t->shards.size(); ++k)
             cuda_check(cudaMemcpyAsync(t->shards[k].amps, c->shards[k].amps,
                                        t->local_len * sizeof(double2), cudaMemcpyDeviceToDevice,
@@ -1042,6 +1044,55 @@ int qgpuDeviceMaxQubits(unsigned long long deviceBytes, int rankLog2, unsigned l
                         int density) {
     return guarded("qgpuDeviceMaxQubits", -1, [&] {
         return qgpu::device_max_qubits(deviceBytes, rankLog2, chunkAmps, density != 0);
+    });
+}
+
+void qgpuSetQubitSwaps(QuESTEnv env, int enable) {
+    guarded_void("qgpuSetQubitSwaps", [&] {
+        Env* e = env_of(env);
+        for (QuregImpl* q : e->quregs) q->restore_identity();
+        e->qubit_swaps = enable != 0;
+    });
+}
+
+int qgpuPlanSwaps(int flatQubits, int rankLog2, unsigned long long chunkAmps, int numOps,
+                  const int* targets, const int* pairOps, int* swapsOut, int maxSwaps) {
+    return guarded("qgpuPlanSwaps", -1, [&] {
+        if (flatQubits < 1 || rankLog2 < 1 || rankLog2 >= flatQubits || numOps < 0)
+            throw qgpu::DomainError("invalid swap-plan request");
+        qgpu::SwapPlanner sp;
+        const int local = flatQubits - rankLog2;
+        sp.reset(flatQubits, local, chunkAmps);
+        std::vector<int> need(static_cast<size_t>(numOps), -1);
+        for (int k = 0; k < numOps; ++k) {
+            if (targets[k] < 0 || targets[k] >= flatQubits) throw qgpu::DomainError("target out of range");
+            if (pairOps[k]) need[k] = targets[k]; // diagonal ops never move
+        }
+        // the runtime's windowing (QuregImpl::enqueue / drain): ops are
+        // planned when kSwapWindow are buffered (the first half) or at a flush
+        int n = 0;
+        size_t begin = 0, end = 0;
+        const size_t total = static_cast<size_t>(numOps);
+        while (begin < total) {
+            end = std::min(total, begin + qgpu::kSwapWindow);
+            const size_t count = end == total ? end - begin : qgpu::kSwapWindow / 2;
+            for (size_t i = begin; i < begin + count; ++i) {
+                if (need[i] < 0) continue;
+                sp.touch(need[i]);
+                const int p = sp.l2p[need[i]];
+                if (p < local) continue;
+                const int v = sp.victim(0, need.data() + i + 1, nullptr, end - i - 1);
+                if (swapsOut && n < maxSwaps) {
+                    swapsOut[3 * n] = static_cast<int>(i);
+                    swapsOut[3 * n + 1] = p;
+                    swapsOut[3 * n + 2] = v;
+                }
+                sp.apply(p, v);
+                ++n;
+            }
+            begin += count;
+        }
+        return n;
     });
 }
 

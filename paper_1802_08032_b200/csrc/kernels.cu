@@ -230,7 +230,8 @@ __global__ void k_depolarise(double2* __restrict__ amps, uint64_t count, int t, 
     const uint64_t row = uint64_t{1} << t, col = uint64_t{1} << tN;
     for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < count;
          u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
-        const uint64_t n00 = insert_zero_bit(insert_zero_bit(u, t), tN);
+        // the two bits in either order (the swap layer may permute them)
+        const uint64_t n00 = insert_zero_bit(insert_zero_bit(u, t < tN ? t : tN), t < tN ? tN : t);
         const uint64_t n11 = n00 | row | col;
         const double2 d0 = amps[n00], d1 = amps[n11];
         amps[n00] = make_double2(fma(swap, d1.x, keep * d0.x), fma(swap, d1.y, keep * d0.y));

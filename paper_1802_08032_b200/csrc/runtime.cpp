@@ -164,6 +164,7 @@ QuregImpl* create_register(Env* env, int N, bool density) {
         cudaGetLastError();
         throw ResourceError("failed to allocate reduction scratch");
     }
+    q->sp.reset(flat, q->local_qubits, env->chunk_amps);
     q->fill_zero();
     if (q->shards[0].rank == 0) {
         const double2 one = make_double2(1.0, 0.0);
@@ -189,10 +190,11 @@ QuregImpl::~QuregImpl() {
 }
 
 void QuregImpl::fill_zero() {
-    discard();
+    discard_all();
     for (auto& s : shards)
         cuda_check(cudaMemsetAsync(s.amps, 0, local_len * sizeof(double2), env->stream),
                    "cudaMemsetAsync");
+    sp.reset(flat, local_qubits, env->chunk_amps); // the whole state is rewritten
 }
 
 void QuregImpl::ensure_recv(uint64_t len) {
@@ -255,44 +257,96 @@ bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
     return true;
 }
 
-void QuregImpl::enqueue(const FlatOp& op) {
+void QuregImpl::enqueue(const FlatOp& lop) {
+    if (!swaps_on()) {
+        enqueue_phys(lop);
+        return;
+    }
+    lq.push_back(lop);
+    if (lq.size() >= kSwapWindow) drain(kSwapWindow / 2);
+}
+
+// Logical ops -> physical: a pair target (and both qubits of a depolarising
+// channel) must be local, so a global one is swapped in first, evicting the
+// local qubit next needed furthest ahead in the buffered window; diagonal
+// ops, dephasing, collapse and controls work on any position.
+void QuregImpl::drain(size_t count) {
+    count = std::min(count, lq.size());
+    std::vector<int> need0(lq.size(), -1), need1(lq.size(), -1);
+    for (size_t j = 0; j < lq.size(); ++j) {
+        const FlatOp& o = lq[j];
+        if (o.kind == FK_GATE && o.cls != CLS_DIAG) need0[j] = o.q0;
+        if (o.kind == FK_DEPOL) {
+            need0[j] = o.q0;
+            need1[j] = o.q1;
+        }
+    }
+    for (size_t i = 0; i < count; ++i) {
+        const FlatOp& lop = lq[i];
+        if (need0[i] >= 0) sp.touch(need0[i]);
+        if (need1[i] >= 0) sp.touch(need1[i]);
+        auto make_local = [&](int logical, uint64_t busy) {
+            const int p = sp.l2p[logical];
+            if (p < local_qubits) return;
+            const size_t nf = lq.size() - i - 1;
+            const int v = sp.victim(busy, need0.data() + i + 1, need1.data() + i + 1, nf);
+            run_swap(p, v);
+            sp.apply(p, v);
+        };
+        if (need0[i] >= 0) make_local(need0[i], 0);
+        if (need1[i] >= 0) make_local(need1[i], uint64_t{1} << sp.l2p[need0[i]]);
+        FlatOp op = lop;
+        op.q0 = sp.phys(lop.q0);
+        op.q1 = sp.phys(lop.q1);
+        op.cmask = sp.phys_mask(lop.cmask);
+        enqueue_phys(op);
+    }
+    lq.erase(lq.begin(), lq.begin() + static_cast<std::ptrdiff_t>(count));
+}
+
+void QuregImpl::enqueue_phys(const FlatOp& op) {
     const bool pair = op.kind == FK_GATE && op.cls != CLS_DIAG;
     if (op.kind == FK_DEPOL) {
-        flush();
+        flush_pass();
         run_depol(op);
         return;
     }
     if (pair && op.q0 >= local_qubits) {
-        flush();
+        flush_pass();
         run_exchange_gate(op);
         return;
     }
     if (env->fusion_mode == 2 || pass_H() < 1) {
-        flush();
+        flush_pass();
         run_simple(op);
         ++passes;
         return;
     }
     if (use_tile()) {
         if (!place_tile(op, pair)) {
-            flush();
+            flush_pass();
             place_tile(op, pair);
         }
         if (env->fusion_mode == 1 ||
             static_cast<int>(pending.size()) >= std::min(env->max_ops, kMaxTileOps))
-            flush();
+            flush_pass();
         return;
     }
     if (pair && op.q0 >= kLaneQubits &&
         std::find(regs.begin(), regs.end(), op.q0) == regs.end()) {
-        if (static_cast<int>(regs.size()) >= pass_H()) flush();
+        if (static_cast<int>(regs.size()) >= pass_H()) flush_pass();
         regs.push_back(op.q0);
     }
     pending.push_back(op);
-    if (env->fusion_mode == 1 || static_cast<int>(pending.size()) >= env->max_ops) flush();
+    if (env->fusion_mode == 1 || static_cast<int>(pending.size()) >= env->max_ops) flush_pass();
 }
 
 void QuregImpl::flush() {
+    if (!lq.empty()) drain(lq.size());
+    flush_pass();
+}
+
+void QuregImpl::flush_pass() {
     if (!pending.empty()) {
         if (use_tile() && env->fusion_mode != 2)
             launch_tile();
@@ -682,6 +736,112 @@ void QuregImpl::run_depol(const FlatOp& op) {
     ++passes;
 }
 
+// ------------------------------------------------------------ qubit swaps
+
+// Trade physical global position g (rank bit j = g - local) with local
+// position v: rank r (bit j = a) keeps the amplitudes whose local bit v is a
+// and trades the half with bit v = !a with partner r ^ 2^j; both sides send
+// and receive the same local offsets (a pure copy, in sub-chunks of
+// min(chunk, 2^v) contiguous amplitudes, double-buffered like the exchange
+// gates).
+void QuregImpl::run_swap(int g, int v) {
+    flush_pass(); // queued ops (e.g. restore_identity's local swaps) run first
+    const int j = g - local_qubits;
+    const uint64_t block = uint64_t{1} << v;
+    const uint64_t unit = std::min<uint64_t>(std::min<uint64_t>(env->chunk_amps, block), local_len / 2);
+    const uint64_t units = (local_len / 2) / unit;
+    ensure_recv(unit);
+    const uint64_t bytes = unit * sizeof(double2);
+    // offset of the u-th unit of the half whose bit v == side
+    auto offset = [&](uint64_t u, int side) {
+        const uint64_t e = u * unit;                      // element index within the half
+        const uint64_t hi = e >> v, lo = e & (block - 1); // deposit a zero... then set bit v
+        return (hi << (v + 1)) | (static_cast<uint64_t>(side) << v) | lo;
+    };
+    ProfScope prof(env, PK_SWAP);
+    if (env->mode == Mode::Nccl) {
+        Shard& s = shards[0];
+        const int a = (s.rank >> j) & 1;
+        const int peer = s.rank ^ (1 << j);
+        ExchangeEvents ev;
+        cuda_check(cudaEventRecord(ev.start, env->stream), "event");
+        cuda_check(cudaStreamWaitEvent(env->comm_stream, ev.start, 0), "event");
+        for (uint64_t u = 0; u < units; ++u) {
+            const int b = static_cast<int>(u & 1);
+            double2* mine = s.amps + offset(u, a ^ 1);
+            if (u >= 2) cuda_check(cudaStreamWaitEvent(env->comm_stream, ev.done[b], 0), "event");
+            env->nccl->sendrecv(peer, mine, recv[b], bytes, env->comm_stream);
+            cuda_check(cudaEventRecord(ev.recv[b], env->comm_stream), "event");
+            cuda_check(cudaStreamWaitEvent(env->stream, ev.recv[b], 0), "event");
+            cuda_check(cudaMemcpyAsync(mine, recv[b], bytes, cudaMemcpyDeviceToDevice, env->stream),
+                       "swap");
+            cuda_check(cudaEventRecord(ev.done[b], env->stream), "event");
+            s.messages += 1;
+            s.bytes += bytes;
+        }
+    } else {
+        for (auto& s : shards) {
+            const int peer = s.rank ^ (1 << j);
+            if (peer < s.rank) continue;
+            Shard& p = shards[peer];
+            // s has bit j = 0 (trades its bit-v = 1 half), p has bit j = 1
+            for (uint64_t u = 0; u < units; ++u) {
+                double2* x = s.amps + offset(u, 1);
+                double2* y = p.amps + offset(u, 0);
+                cuda_check(cudaMemcpyAsync(recv[0], x, bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
+                cuda_check(cudaMemcpyAsync(x, y, bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
+                cuda_check(cudaMemcpyAsync(y, recv[0], bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
+                s.messages += 1;
+                s.bytes += bytes;
+                p.messages += 1;
+                p.bytes += bytes;
+            }
+        }
+    }
+    ++passes;
+}
+
+// Swap two local qubits with three CNOTs (pure amplitude moves: exact).
+void QuregImpl::local_swap(int a, int b) {
+    FlatOp x;
+    x.kind = FK_GATE;
+    x.m[2] = 1.0;
+    x.m[4] = 1.0;
+    x.cls = classify(x.m, &x.flags);
+    for (int k = 0; k < 3; ++k) {
+        x.q0 = k == 1 ? a : b;
+        x.cmask = uint64_t{1} << (k == 1 ? b : a);
+        enqueue_phys(x);
+    }
+}
+
+void QuregImpl::restore_identity() {
+    if (!swaps_on()) return;
+    flush(); // drain the logical queue first: it may swap
+    if (sp.identity()) return;
+    for (int L = 0; L < flat; ++L) {
+        const int P = sp.l2p[L], Q = L; // current and home position
+        if (P == Q) continue;
+        const bool pg = P >= local_qubits, qg = Q >= local_qubits;
+        if (!pg && !qg) {
+            local_swap(P, Q);
+        } else if (pg != qg) {
+            run_swap(pg ? P : Q, pg ? Q : P);
+        } else { // both global: (P w)(Q w)(P w) = (P Q) through a local w
+            const int w = sp.victim(0);
+            run_swap(P, w);
+            sp.apply(P, w);
+            run_swap(Q, w);
+            sp.apply(Q, w);
+            run_swap(P, w);
+            sp.apply(P, w);
+            continue;
+        }
+        sp.apply(P, Q);
+    }
+    flush_pass();
+}
+
 // -------------------------------------------------------------- reductions
 
 namespace {
@@ -719,6 +879,7 @@ double QuregImpl::combine_results(int n) {
 
 double QuregImpl::reduce_norm(int t, int outcome) {
     flush();
+    if (swaps_on()) t = sp.phys(t);
     ProfScope prof(env, PK_REDUCE);
     for (size_t k = 0; k < shards.size(); ++k)
         launch_reduce_norm(shards[k].amps, local_len, goff(shards[k]), t, outcome, partials,
@@ -728,6 +889,7 @@ double QuregImpl::reduce_norm(int t, int outcome) {
 }
 
 double QuregImpl::reduce_diag(int t, int outcome, int comp) {
+    restore_identity(); // the diagonal is j == k in the logical layout
     flush();
     ProfScope prof(env, PK_REDUCE);
     for (size_t k = 0; k < shards.size(); ++k)
@@ -746,6 +908,7 @@ Complex QuregImpl::trace() {
 }
 
 void QuregImpl::get_flat(uint64_t start, uint64_t num, double2* out) {
+    restore_identity();
     flush();
     const uint64_t end = start + num;
     if (env->mode == Mode::Nccl && env->num_ranks > 1) {
@@ -791,6 +954,7 @@ void QuregImpl::get_flat(uint64_t start, uint64_t num, double2* out) {
 }
 
 void QuregImpl::set_flat(uint64_t start, uint64_t num, const double2* in) {
+    restore_identity();
     flush();
     const uint64_t end = start + num;
     for (auto& s : shards) {

@@ -6,6 +6,7 @@
 #include "QuEST.h"
 #include "qgpu.h"
 #include "qgpu_device.h"
+#include "swap_plan.h"
 
 #include <cuda_runtime.h>
 
@@ -56,6 +57,9 @@ struct Env {
     int tile_targets = kTileHigh; // distinct pair targets above qubit 4 per pass
     int tile_phases = 2;          // register phases per pass
     uint64_t chunk_amps = uint64_t{1} << 24;
+    // global<->local qubit swaps instead of per-gate exchanges (swap_plan.h);
+    // qgpuSetQubitSwaps turns them off (the reference's exchange per gate)
+    bool qubit_swaps = true;
     std::unique_ptr<NcclComm> nccl;
     std::set<struct QuregImpl*> quregs;
 
@@ -73,7 +77,7 @@ struct Env {
     ~Env();
 };
 
-enum ProfKind { PK_PASS = 0, PK_SIMPLE = 1, PK_EXCHANGE = 2, PK_DEPOL = 3, PK_REDUCE = 4 };
+enum ProfKind { PK_PASS = 0, PK_SIMPLE = 1, PK_EXCHANGE = 2, PK_DEPOL = 3, PK_REDUCE = 4, PK_SWAP = 5 };
 
 // Brackets the enclosed launches with an event pair when profiling is on.
 class ProfScope {
@@ -135,10 +139,27 @@ struct QuregImpl {
     std::vector<int> tile_high;      // tile pass: high qubits in the tile
     std::vector<PhaseState> phases;  // tile pass: phases
 
+    // logical -> physical qubit map (global<->local swaps, swap_plan.h)
+    SwapPlanner sp;
+
     ~QuregImpl();
 
+    // queue an op on LOGICAL qubits: maps it through the swap planner (and
+    // swaps a global target in first), then enqueue_phys
     void enqueue(const FlatOp& op);
+    void enqueue_phys(const FlatOp& op);
+    std::vector<FlatOp> lq;       // logical ops awaiting swap planning
+    void drain(size_t count);     // plan + enqueue_phys the first `count` of lq
+    void flush_pass();            // launch the open pass
+    bool swaps_on() const { return env->qubit_swaps && env->rank_log2 > 0; }
+    // move every logical qubit back to its own position (before amplitudes
+    // are read or written by index)
+    void restore_identity();
     void flush();
+    void discard_all() { // queued ops are dead (the state is overwritten)
+        lq.clear();
+        discard();
+    }
     void discard() {
         pending.clear();
         regs.clear();
@@ -164,6 +185,8 @@ struct QuregImpl {
     void launch_fused();
     void run_exchange_gate(const FlatOp& op);
     void run_depol(const FlatOp& op);
+    void run_swap(int g, int v); // trade physical global position g with local v
+    void local_swap(int a, int b);
     void ensure_recv(uint64_t len);
     uint64_t goff(const Shard& s) const { return static_cast<uint64_t>(s.rank) * local_len; }
     double combine_results(int n); // rank-ordered double-double sum

@@ -154,6 +154,8 @@ _SIGS = {
     "qgpuNormSquared": (_D, [Qureg]),
     "qgpuTrace": (Complex, [Qureg]),
     "qgpuSetExchangeChunk": (None, [QuESTEnv, _LL]),
+    "qgpuSetQubitSwaps": (None, [QuESTEnv, _I]),
+    "qgpuPlanSwaps": (_I, [_I, _I, _ULL, _I, _VP, _VP, _VP, _I]),
     "qgpuCommStats": (None, [Qureg, _VP, _VP]),
     "qgpuPlanGate": (_I, [_I, _I, _I, _I, _ULL, _IP, _IP, ctypes.POINTER(ctypes.c_ulonglong)]),
     "qgpuPlanChunks": (_I, [_ULL, _ULL, ctypes.POINTER(ctypes.c_ulonglong)]),
@@ -263,6 +265,11 @@ class Env:
 
     def set_exchange_chunk(self, amps: int):
         call("qgpuSetExchangeChunk", self.h, amps)
+
+    def set_qubit_swaps(self, enable: bool):
+        """Global<->local qubit swaps (True, default) or the reference's
+        exchange per global-target gate (False)."""
+        call("qgpuSetQubitSwaps", self.h, int(enable))
 
     @property
     def stream(self) -> int:
@@ -413,3 +420,17 @@ def device_max_qubits(device_bytes: int, k: int, chunk_amps: int = 1 << 24, dens
     if r < 0:
         check()
     return r
+
+
+def plan_swaps(flat: int, rank_log2: int, ops, chunk_amps: int = 1 << 24):
+    """qgpuPlanSwaps over [(target, is_pair), ...]: [(op index, global pos, local pos)]."""
+    import numpy as np
+
+    t = np.array([o[0] for o in ops], dtype=np.int32)
+    pr = np.array([int(o[1]) for o in ops], dtype=np.int32)
+    out = np.zeros(3 * max(1, len(ops)), dtype=np.int32)
+    n = lib().qgpuPlanSwaps(flat, rank_log2, chunk_amps, len(ops), t.ctypes.data, pr.ctypes.data,
+                            out.ctypes.data, len(ops))
+    if n < 0:
+        check()
+    return [tuple(int(x) for x in out[3 * i:3 * i + 3]) for i in range(n)]

@@ -191,12 +191,69 @@ def test_loopback_distributed_equals_single(k, density):
         env.destroy()
 
 
+@pytest.mark.parametrize("k", [1, 2, 3])
+@pytest.mark.parametrize("density", [False, True])
+@pytest.mark.parametrize("chunk", [16, 1 << 24])
+def test_qubit_swaps_equal_single(k, density, chunk):
+    """Global<->local swaps (default) give the single-rank result bit for bit,
+    including reductions, collapse and amplitude reads taken while qubits are
+    displaced."""
+    n = 4 if density else 11
+    c = random_gate_circuit(n, 160, seed=90 + k, max_controls=2, channels=density)
+    want = oracle_run(c, density=density)
+    env = quest.Env.loopback(1 << k)
+    env.set_exchange_chunk(chunk)
+    try:
+        q = quest.QuregHandle(env, n, density)
+        C.apply_circuit(q, c)
+        flat = 2 * n if density else n
+        # probabilities before any read restores the layout
+        for t in range(n):
+            want_p = oracle.orc_prob_of_outcome(want, n, t, 1, density)
+            assert abs(q.calcProbOfOutcome(t, 1) - want_p) < TOL
+        a = q.getAmp(5) if not density else None
+        got = q.state()
+        assert_parity(got, want)
+        if a is not None:
+            assert a.real == want[5].real and a.imag == want[5].imag
+        # keep going from a restored layout, then collapse while displaced
+        C.apply_circuit(q, c)
+        want2 = oracle_run(c, density=density, init=want)
+        t = n - 1
+        p = oracle.orc_prob_of_outcome(want2, n, t, 0, density)
+        q.collapseToOutcome(t, 0)
+        want3 = oracle.orc_collapse(want2, n, t, 0, p, density)
+        assert np.max(np.abs(q.state() - want3)) < TOL
+        q.destroy()
+    finally:
+        env.destroy()
+
+
+def test_qubit_swaps_cut_exchange_traffic():
+    """A layer of gates on the global qubits: per-gate exchanges move a whole
+    partition per gate; swaps move half a partition once per qubit."""
+    n, k = 12, 2
+    c = C.layered_random_circuit(n, 6, 5)
+    traffic = {}
+    for swaps in (False, True):
+        env = quest.Env.loopback(1 << k)
+        env.set_qubit_swaps(swaps)
+        q = quest.QuregHandle(env, n)
+        C.apply_circuit(q, c)
+        q.flush()
+        traffic[swaps] = int(q.comm_stats(1 << k)[1].sum())
+        q.destroy()
+        env.destroy()
+    assert 0 < traffic[True] < traffic[False] / 2, traffic
+
+
 def test_loopback_comm_accounting():
     """Exchange accounting: a communicated gate moves exactly
     16 * 2^(n-k) bytes per rank, in 2^(n-k)/chunk messages; local gates none."""
     n, k = 10, 2
     env = quest.Env.loopback(1 << k)
     env.set_exchange_chunk(64)
+    env.set_qubit_swaps(False)  # the reference's exchange per gate
     q = quest.QuregHandle(env, n)
     q.hadamard(3)
     q.flush()
