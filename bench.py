@@ -265,7 +265,8 @@ def run_ours(args):
     except Exception:
         pass
     pass_ms = ms_launch[kinds == 0]
-    exch_ms = ms_launch[kinds == 2]
+    exch_ms = ms_launch[kinds == 2]  # per-gate exchanges (swaps off)
+    swap_ms = ms_launch[kinds == 5]  # global<->local qubit swaps
     per_launch_bytes = 2.0 * 16.0 * (2.0 ** args.local_qubits)
     achieved = per_launch_bytes / (float(pass_ms.mean()) / 1e3) / 1e9 if pass_ms.size else None
     share = float(pass_ms.sum()) / float(ms_launch.sum()) if ms_launch.size else None
@@ -328,9 +329,17 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "cpu_baseline": cpu,
         }
-        if exch_ms.size:
-            nv = 16.0 * (2.0 ** args.local_qubits) / (float(exch_ms.mean()) / 1e3) / 1e9
-            line["nvlink"] = {"exchange_gates": int(exch_ms.size), "avg_ms": round(float(exch_ms.mean()), 3),
+        if exch_ms.size or swap_ms.size:
+            # bytes each way per rank: a whole partition per exchange gate,
+            # half a partition per qubit swap
+            part = 16.0 * (2.0 ** args.local_qubits)
+            moved = part * exch_ms.size + 0.5 * part * swap_ms.size
+            t_s = (float(exch_ms.sum()) + float(swap_ms.sum())) / 1e3
+            nv = moved / t_s / 1e9
+            line["nvlink"] = {"exchange_gates": int(exch_ms.size) // args.steps,
+                              "qubit_swaps": int(swap_ms.size) // args.steps,
+                              "bytes_per_direction_per_step": int(moved / args.steps),
+                              "avg_ms": round(t_s * 1e3 / max(1, exch_ms.size + swap_ms.size), 3),
                               "GBps_per_direction": round(nv, 1), "frac_of_900": round(nv / 900.0, 4)}
         print(json.dumps(line), flush=True)
     q.destroy()

@@ -345,3 +345,64 @@ def test_30q_forward_inverse_property(env):
     assert abs(a0.real - 1.0) < 1e-12 and abs(a0.imag) < 1e-12
     assert abs(q.calcProbOfOutcome(n - 1, 0) - 1.0) < 1e-12
     q.destroy()
+
+
+@pytest.mark.slow
+def test_33q_config_c3a_forward_inverse(env):
+    """Config C3a size (33 qubits = 128 GiB on one B200): a layered circuit
+    and its inverse return |0>, the norm stays 1 (size-independent)."""
+    n = 33
+    c = C.layered_random_circuit(n, 2, 12345)
+    q = quest.QuregHandle(env, n)
+    try:
+        C.apply_circuit(q, c)
+        assert abs(q.calcTotalProb() - 1.0) < 1e-12
+        C.apply_circuit(q, C.inverse_circuit(c))
+        a0 = q.getAmp(0)
+        assert abs(a0.real - 1.0) < 1e-12 and abs(a0.imag) < 1e-12
+        assert abs(q.calcProbOfOutcome(n - 1, 1)) < 1e-12
+    finally:
+        q.destroy()
+
+
+@pytest.mark.slow
+def test_32q_config_c5_qft_measure_collapse(env):
+    """Config C5 size (32 qubits): QFT of a basis state with multi-controlled
+    phase flips; every qubit then reads P = 1/2 and collapsing four of them
+    leaves a normalised state with those outcomes certain."""
+    n = 32
+    q = quest.QuregHandle(env, n)
+    try:
+        q.initClassicalState(0x5A5A5A5A)
+        C.apply_circuit(q, C.qft_circuit(n, mcpf_every=3))
+        for t in range(n):
+            assert abs(q.calcProbOfOutcome(t, 0) - 0.5) < 1e-12
+        for t, o in [(0, 1), (9, 0), (21, 1), (31, 0)]:
+            assert abs(q.collapseToOutcome(t, o) - 0.5) < 1e-12
+        assert abs(q.calcTotalProb() - 1.0) < 1e-12
+        for t, o in [(0, 1), (9, 0), (21, 1), (31, 0)]:
+            assert abs(q.calcProbOfOutcome(t, o) - 1.0) < 1e-12
+        assert abs(q.calcProbOfOutcome(5, 0) - 0.5) < 1e-12
+    finally:
+        q.destroy()
+
+
+@pytest.mark.slow
+@pytest.mark.skipif(not oracle.ref_available(), reason="compiled reference not present")
+def test_14q_density_config_c4_against_reference(env):
+    """Config C4 size (14-qubit density matrix = 28-qubit vector, 4 GiB):
+    a noisy layered circuit, bit-identical to the compiled reference run with
+    all host threads; trace 1 and purity below 1."""
+    import os
+
+    N = 14
+    c = C.layered_random_circuit(N, 1, 7, noise_pmax=0.1)
+    want = oracle.ref_run(N, to_oracle_ops(c), density=True, workers=os.cpu_count() or 1)
+    q = quest.QuregHandle(env, N, density=True)
+    try:
+        C.apply_circuit(q, c)
+        assert abs(q.calcTotalProb() - 1.0) < 1e-12
+        assert q.calcPurity() < 1.0
+        assert_parity(q.state(), want)
+    finally:
+        q.destroy()
