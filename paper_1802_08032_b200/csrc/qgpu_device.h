@@ -177,6 +177,8 @@ struct TileParams {
     int32_t high_pos[kTileHigh];           // ascending global qubits of tile bits 5..
     int32_t any_outer;                     // some op has controls outside the tile
     uint64_t seg_off[1 << kTileHigh];      // global offset of tile segment s
+    // the 8 segments warp w owns in the last phase (its warp bits fixed)
+    uint8_t fin_seg[1 << kTileWarpBits][1 << (kTileHigh - kTileWarpBits)];
     TilePhase phases[kMaxPhases];
     TileOp ops[kMaxTileOps];
 };

@@ -413,6 +413,24 @@ void QuregImpl::launch_tile() {
             Q.warp_off[w] = static_cast<uint16_t>(off);
         }
         for (int j = 0; j < 2; ++j) Q.lane_off[j] = static_cast<uint16_t>(1u << lb[j]);
+        if (p + 1 == phases.size()) {
+            // last phase: warp w owns the segments whose warp bits are w
+            // (tile bits 0-4 are lane or register bits, never warp bits)
+            std::vector<int> free_hi;
+            for (int t = kLaneQubits; t < kTileQubits; ++t)
+                if (std::find(wb.begin(), wb.end(), t) == wb.end()) free_hi.push_back(t - kLaneQubits);
+            for (int w = 0; w < (1 << kTileWarpBits); ++w) {
+                uint32_t base = 0;
+                for (int j = 0; j < kTileWarpBits; ++j)
+                    if ((w >> j) & 1) base |= 1u << (wb[j] - kLaneQubits);
+                for (int i = 0; i < (1 << (kTileHigh - kTileWarpBits)); ++i) {
+                    uint32_t sg = base;
+                    for (size_t j = 0; j < free_hi.size(); ++j)
+                        if ((i >> j) & 1) sg |= 1u << free_hi[j];
+                    P.fin_seg[w][i] = static_cast<uint8_t>(sg);
+                }
+            }
+        }
         const int begin = phases[p].op_begin;
         const int end = p + 1 < phases.size() ? phases[p + 1].op_begin : static_cast<int>(pending.size());
         Q.op_begin = static_cast<uint16_t>(begin);

@@ -467,34 +467,40 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
         return g;
     };
 
-    // runs of 2^seg_run segments are contiguous in HBM: one bulk copy each,
-    // spread over the threads. The expected byte count may be posted after
-    // other threads' copies completed: the tx-count goes negative meanwhile
-    // and the phase cannot complete before thread 0's arrival.
-    const int run = P.seg_run;
-    auto copies = [&](uint64_t t, bool load) {
+    // Each warp owns 8 whole 512-byte segments of the tile in the last phase
+    // (tile bits 0-4 are never warp bits, so a warp's amplitudes there are
+    // the segments with its own warp bits: P.fin_seg[w]). It stores them and
+    // refills their slots itself — lanes 0-7 one bulk copy each, lane 0
+    // posting the warp's 4 KiB on the stage's tx-count mbarrier (16
+    // arrivals per fill) — so no block barrier separates tiles.
+    constexpr uint32_t SEG_BYTES = 32u * sizeof(double2);
+    const uint32_t my_seg = lane < 8 ? P.fin_seg[w][lane] : 0;
+    auto load_mine = [&](uint64_t t) {
         const int b = static_cast<int>(t % NBUF);
         const uint64_t gb = tile_gbase(blockIdx.x + t * G);
         double2* buf = smem + (static_cast<size_t>(b) << K);
-        if (load && threadIdx.x == 0) mbar_expect_tx(&full[b], TILE_BYTES);
-        for (int sg = static_cast<int>(threadIdx.x) << run; sg < NSEG; sg += blockDim.x << run) {
-            if (load)
-                tma_load(buf + (sg << kLaneQubits), amps + gb + P.seg_off[sg],
-                         (32u * sizeof(double2)) << run, &full[b]);
-            else
-                tma_store(amps + gb + P.seg_off[sg], buf + (sg << kLaneQubits),
-                          (32u * sizeof(double2)) << run);
+        if (lane < 8)
+            tma_load(buf + (my_seg << kLaneQubits), amps + gb + P.seg_off[my_seg], SEG_BYTES, &full[b]);
+        if (lane == 0) mbar_expect_tx(&full[b], 8 * SEG_BYTES);
+    };
+    auto store_mine = [&](uint64_t t) {
+        const int b = static_cast<int>(t % NBUF);
+        const uint64_t gb = tile_gbase(blockIdx.x + t * G);
+        double2* buf = smem + (static_cast<size_t>(b) << K);
+        if (lane < 8) {
+            tma_store(amps + gb + P.seg_off[my_seg], buf + (my_seg << kLaneQubits), SEG_BYTES);
+            tma_commit();
         }
     };
 
     if (threadIdx.x == 0) {
-        for (int b = 0; b < NBUF; ++b) mbar_init(&full[b], 1);
+        for (int b = 0; b < NBUF; ++b) mbar_init(&full[b], 1u << WB);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     for (int k = threadIdx.x; k < kGbaseChunks * 256; k += blockDim.x)
         gtab[k >> 8][k & 255] = tile_gbase_slow<RB, WB>(P, static_cast<uint64_t>(k & 255) << (8 * (k >> 8)));
     __syncthreads();
-    for (uint64_t t = 0; t < NBUF && t < ntiles; ++t) copies(t, true);
+    for (uint64_t t = 0; t < NBUF && t < ntiles; ++t) load_mine(t);
     const int nops = P.phases[nph - 1].op_end;
     const uint32_t sops_addr = smem_u32(sops);
     {
@@ -512,14 +518,19 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
         const uint64_t gbase = tile_gbase(blockIdx.x + t * G) + P.global_offset;
         const uint64_t act = any_outer ? active_ops(sops, nops, gbase, lane) : ~uint64_t{0};
         mbar_wait(&full[b], static_cast<uint32_t>((t / NBUF) & 1));
+        bool wrote = false, last_skipped = false; // (uniform per tile)
         for (int ph = 0; ph < nph; ++ph) {
             const TilePhase& Q = P.phases[ph];
             const int end = Q.op_end;
             uint64_t m = act & ((uint64_t{1} << end) - 1) &
                          ~((uint64_t{1} << Q.op_begin) - 1);
-            if (m == 0) continue; // no op runs: the tile stays as it is in shared memory
+            if (m == 0) { // no op runs: the tile stays as it is in shared memory
+                last_skipped = ph == nph - 1;
+                continue;
+            }
             // end < 64 always: kMaxTileOps entries plus the sentinel
-            if (ph > 0) __syncthreads(); // previous phase's writes are in
+            if (wrote) __syncthreads(); // the previous phase's writes are in
+            wrote = true;
             const uint32_t wofs = Q.warp_off[w] + (lane & 7u) + ((lane >> 3) & 1u ? Q.lane_off[0] : 0u) +
                                   ((lane >> 4) & 1u ? Q.lane_off[1] : 0u);
             double2 a[R], b[R];
@@ -554,14 +565,19 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
                 }
             }
         }
+        // the warp's segments hold its own last-phase writes — unless the
+        // last phase was skipped on this tile after an earlier one wrote
+        // (rare: outer controls); then other warps wrote them
+        if (last_skipped && wrote) __syncthreads();
         fence_proxy_async(); // generic-proxy writes -> visible to the bulk store
-        tma_wait_read<0>();  // own part of the store of tile t - 1 has left its stage
-        __syncthreads();
-        copies(t, false);
-        tma_commit();
-        if (t >= 1 && t - 1 + NBUF < ntiles) copies(t - 1 + NBUF, true);
+        __syncwarp();
+        store_mine(t);
+        if (t >= 1 && t - 1 + NBUF < ntiles) {
+            if (lane < 8) tma_wait_read<1>(); // the store of tile t - 1 left the slot
+            load_mine(t - 1 + NBUF);
+        }
     }
-    tma_wait_all();
+    if (lane < 8) tma_wait_all();
 }
 
 } // namespace
