@@ -21,6 +21,8 @@
 #include "transport.h"
 
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 namespace qgpu {
@@ -356,6 +358,41 @@ void QuregImpl::flush_pass() {
     discard();
 }
 
+// QGPU_PASS_STATS=1: histogram of tile-pass handler codes and phase counts,
+// printed at exit (scheduler / kernel tuning aid; off by default).
+namespace {
+struct PassStats {
+    uint64_t passes = 0, phases = 0, ops = 0, outer = 0;
+    uint64_t code[64] = {};
+    ~PassStats() {
+        if (!passes) return;
+        std::fprintf(stderr, "[qgpu pass stats] passes %llu, phases/pass %.2f, ops/pass %.2f, outer-controlled %.1f%%\n",
+                     (unsigned long long)passes, double(phases) / passes, double(ops) / passes,
+                     100.0 * double(outer) / double(ops ? ops : 1));
+        for (int c = 0; c < 64; ++c)
+            if (code[c])
+                std::fprintf(stderr, "  code %2d: %6.2f per pass\n", c, double(code[c]) / passes);
+    }
+};
+PassStats g_pass_stats;
+} // namespace
+
+bool pass_stats_enabled() {
+    static const bool on = std::getenv("QGPU_PASS_STATS") != nullptr;
+    return on;
+}
+
+void record_pass_stats(const TileParams& P) {
+    const int nops = P.phases[P.num_phases - 1].op_end;
+    ++g_pass_stats.passes;
+    g_pass_stats.phases += P.num_phases;
+    g_pass_stats.ops += nops;
+    for (int k = 0; k < nops; ++k) {
+        ++g_pass_stats.code[P.ops[k].hdr & 63];
+        if (P.ops[k].outer_cmask) ++g_pass_stats.outer;
+    }
+}
+
 void QuregImpl::launch_tile() {
     // The tile's high qubits: the pass's pair targets, topped up with the
     // lowest unused local qubits, so that qubits 5, 6, ... extend the
@@ -523,11 +560,17 @@ void QuregImpl::launch_tile() {
                 }
             }
             to.hdr = tile_hdr(code, flags, op.outcome, q0k, q0p, q1k, q1p, lane_cm, reg_cm, warp_cm);
+            // a diagonal gate with a == 1 exactly (Z, S, T, phase shifts)
+            // on a qubit outside the tile is the identity wherever that bit
+            // is 0: a control on it, so those tiles skip the op
+            if (op.kind == FK_GATE && op.cls == CLS_DIAG && q0k == TL_OUTER && (op.flags & DF_A_ONE))
+                outer |= uint64_t{1} << op.q0;
             to.outer_cmask = outer;
             if (outer) P.any_outer = 1;
             std::memcpy(to.m, op.m, sizeof(to.m));
         }
     }
+    if (pass_stats_enabled()) record_pass_stats(P);
     ProfScope prof(env, PK_PASS);
     for (auto& s : shards) {
         P.global_offset = goff(s);

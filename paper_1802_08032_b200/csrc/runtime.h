@@ -194,6 +194,9 @@ struct QuregImpl {
 
 QuregImpl* create_register(Env* env, int N, bool density);
 
+bool pass_stats_enabled();
+void record_pass_stats(const TileParams& P);
+
 // Pure planner (qgpu.h: qgpuPlanGate).
 // memory_plan.cpp: the reference's node model (distributed.cpp:423-468) and
 // this runtime's per-rank device footprint
