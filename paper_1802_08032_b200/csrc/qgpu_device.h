@@ -167,6 +167,9 @@ struct TilePhase {
     uint16_t warp_off[1 << kTileWarpBits]; // tile index offset of warp w
     uint16_t lane_off[2];                  // tile index offsets of lane bits 3, 4
     uint16_t op_begin, op_end;
+    // warp bits shared with the previous phase at the same (top) positions:
+    // the transition into this phase syncs groups of 2^(WB - sync_bits) warps
+    uint16_t sync_bits;
 };
 
 struct TileParams {

@@ -422,21 +422,101 @@ void QuregImpl::launch_tile() {
             if ((s >> j) & 1) off |= uint64_t{1} << high[j];
         P.seg_off[s] = off;
     }
+    // Per phase: register bits (the phase's targets, topped up), lane bits 3-4
+    // and warp bits (the rest of tile bits 3..11). Layouts are chosen so that
+    // consecutive phases share as many warp bits as possible, at the same
+    // (top) warp-index positions: data then only moves within groups of
+    // 2^(WB - c) warps, which synchronise on a named barrier instead of the
+    // whole CTA (c = shared bits; kernel: TilePhase.sync_bits).
+    const size_t nph = phases.size();
+    std::vector<std::vector<int>> RB(nph), LB(nph), WBv(nph);
+    auto has = [](const std::vector<int>& v, int t) { return std::find(v.begin(), v.end(), t) != v.end(); };
+    for (size_t p = 0; p < nph; ++p)
+        for (int q : phases[p].regs) RB[p].push_back(tbit(q));
+    for (size_t p = nph; p-- > 0;) {
+        std::vector<int> pref; // bits better kept off this phase's warp bits
+        if (p + 1 < nph) {
+            for (int t : RB[p + 1]) pref.push_back(t);
+            for (int t : LB[p + 1]) pref.push_back(t);
+        }
+        const bool last = p + 1 == nph;
+        // top up the register bits: first from `pref`, then the lowest free
+        for (int t : pref)
+            if (static_cast<int>(RB[p].size()) < kPhaseRegBits && t >= kLaneQubits && !has(RB[p], t))
+                RB[p].push_back(t);
+        for (int t = kLaneQubits; t < kTileQubits && static_cast<int>(RB[p].size()) < kPhaseRegBits; ++t)
+            if (!has(RB[p], t)) RB[p].push_back(t);
+        // lane bits 3-4: in the last phase tile bits 3, 4 unless registers
+        // (tile bits 0-4 are never warp bits there: per-warp segments);
+        // earlier phases prefer bits of `pref`
+        if (last) {
+            for (int t = kFixedLaneBits; t < kTileQubits && LB[p].size() < 2; ++t)
+                if (!has(RB[p], t)) LB[p].push_back(t);
+        } else {
+            // qubits 3, 4 targeted by this phase's pair ops (as lane ops,
+            // place_tile) must stay lane bits
+            const int begin = phases[p].op_begin;
+            const int end = phases[p + 1].op_begin;
+            for (int k = begin; k < end; ++k) {
+                const FlatOp& op = pending[k];
+                const bool pair = op.kind == FK_GATE && op.cls != CLS_DIAG;
+                if (pair && op.q0 >= kFixedLaneBits && op.q0 < kLaneQubits && !has(RB[p], op.q0) &&
+                    !has(LB[p], op.q0))
+                    LB[p].push_back(op.q0);
+            }
+            for (int t : pref)
+                if (LB[p].size() < 2 && !has(RB[p], t) && !has(LB[p], t)) LB[p].push_back(t);
+            for (int t = kFixedLaneBits; t < kTileQubits && LB[p].size() < 2; ++t)
+                if (!has(RB[p], t) && !has(LB[p], t)) LB[p].push_back(t);
+        }
+        for (int t = kFixedLaneBits; t < kTileQubits; ++t)
+            if (!has(RB[p], t) && !has(LB[p], t)) WBv[p].push_back(t);
+    }
+    // order warp bits: bits shared with the next phase on top (same order)
+    std::vector<int> sync_bits(nph, 0);
+    for (size_t p = 0; p + 1 < nph; ++p) {
+        std::vector<int> common;
+        for (int t : WBv[p])
+            if (has(WBv[p + 1], t)) common.push_back(t);
+        auto reorder = [&](std::vector<int>& wb, bool keep_top) {
+            std::vector<int> rest;
+            for (int t : wb)
+                if (!has(common, t)) rest.push_back(t);
+            std::vector<int> out = rest;
+            for (int t : common) out.push_back(t);
+            if (keep_top) {
+                // the next phase may already be ordered for its own next
+                // transition: only sync in groups if the positions agree
+                return;
+            }
+            wb = out;
+        };
+        reorder(WBv[p], false);
+        // the next phase: put the common bits at the same top positions
+        // unless that breaks its own (already fixed) order — phases are
+        // processed front to back, so only the first transition of a
+        // 3+-phase pass could be affected; check positions explicitly
+        std::vector<int> rest;
+        for (int t : WBv[p + 1])
+            if (!has(common, t)) rest.push_back(t);
+        std::vector<int> nb = rest;
+        for (int t : common) nb.push_back(t);
+        WBv[p + 1] = nb;
+        (void)reorder;
+    }
+    for (size_t p = 1; p < nph; ++p) {
+        int c = 0;
+        while (c < kTileWarpBits &&
+               WBv[p][kTileWarpBits - 1 - c] == WBv[p - 1][kTileWarpBits - 1 - c])
+            ++c;
+        sync_bits[p] = c;
+    }
     for (size_t p = 0; p < phases.size(); ++p) {
         TilePhase& Q = P.phases[p];
-        // register bits: the phase's targets, then other tile bits; lane bits
-        // 3, 4: qubits 3, 4 unless they are registers, else the lowest free
-        // high bits; warp bits: the rest
-        std::vector<int> rb, lb, wb;
-        for (int q : phases[p].regs) rb.push_back(tbit(q));
-        for (int t = kLaneQubits; t < kTileQubits && static_cast<int>(rb.size()) < kPhaseRegBits; ++t)
-            if (std::find(rb.begin(), rb.end(), t) == rb.end()) rb.push_back(t);
-        for (int t = kFixedLaneBits; t < kTileQubits && lb.size() < 2; ++t)
-            if (std::find(rb.begin(), rb.end(), t) == rb.end()) lb.push_back(t);
-        for (int t = kFixedLaneBits; t < kTileQubits; ++t)
-            if (std::find(rb.begin(), rb.end(), t) == rb.end() &&
-                std::find(lb.begin(), lb.end(), t) == lb.end())
-                wb.push_back(t);
+        const std::vector<int>& rb = RB[p];
+        const std::vector<int>& lb = LB[p];
+        const std::vector<int>& wb = WBv[p];
+        Q.sync_bits = static_cast<uint16_t>(sync_bits[p]);
         for (int i = 0; i < (1 << kPhaseRegBits); ++i) {
             uint32_t off = 0;
             for (int j = 0; j < kPhaseRegBits; ++j)

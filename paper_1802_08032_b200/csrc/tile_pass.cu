@@ -529,7 +529,16 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
                 continue;
             }
             // end < 64 always: kMaxTileOps entries plus the sentinel
-            if (wrote) __syncthreads(); // the previous phase's writes are in
+            if (wrote) { // the previous phase's writes are in (within the group)
+                const int c = Q.sync_bits;
+                if (c == 0)
+                    __syncthreads();
+                else if (c >= WB)
+                    __syncwarp();
+                else
+                    asm volatile("bar.sync %0, %1;" ::"r"(1 + (w >> (WB - c))), "r"(32 << (WB - c))
+                                 : "memory");
+            }
             wrote = true;
             const uint32_t wofs = Q.warp_off[w] + (lane & 7u) + ((lane >> 3) & 1u ? Q.lane_off[0] : 0u) +
                                   ((lane >> 4) & 1u ? Q.lane_off[1] : 0u);
