@@ -58,6 +58,7 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--fusion", type=int, default=0, help="0 fused, 1 pass per op, 2 simple kernels")
     p.add_argument("--reg-qubits", type=int, default=0)
+    p.add_argument("--jit", type=int, default=1, help="per-pass JIT: 0 off, 1 on (background compiles)")
     return p.parse_args()
 
 
@@ -212,6 +213,8 @@ def run_ours(args):
         env = quest.Env()
     if args.fusion or args.reg_qubits:
         env.set_fusion(args.fusion, 0, args.reg_qubits)
+    quest.set_jit(args.jit)
+    jit_wait_s = 0.0
     k = int(math.log2(world))
     n = args.local_qubits + k
     circuit = circuit_for(n, args.depth, args.seed)
@@ -225,10 +228,16 @@ def run_ours(args):
         if dist:
             dist.barrier()
 
-    # warm-up (also compiles nothing: the library is AOT sm_100a)
-    for _ in range(args.warmup):
+    # warm-up: each step queues its new pass shapes for the per-pass JIT
+    # (NVRTC on background threads; the interpreter runs meanwhile) and waits
+    # for those compiles; later steps load and run the compiled kernels
+    for i in range(args.warmup):
         C.apply_circuit(q, circuit)
-    q.flush()
+        q.flush()
+        env.sync()
+        t_jit = time.perf_counter()
+        quest.jit_wait()  # (step junctions cut a few more shapes than step 1)
+        jit_wait_s += time.perf_counter() - t_jit
     barrier()
 
     launches0 = quest.kernel_launches()
@@ -314,7 +323,10 @@ def run_ours(args):
                        "qubits": n, "local_qubits": args.local_qubits, "gates": gates,
                        "parallelism": f"amplitude partition over {world} GPU(s)",
                        "l2": "state 16 GiB per GPU >> 126 MB L2 (no flush needed)",
-                       "passes_per_step": passes / args.steps, "fusion": args.fusion},
+                       "passes_per_step": passes / args.steps, "fusion": args.fusion,
+                       "jit": {"mode": quest.lib().qgpuGetJit(), "kernels": quest.jit_stats()[0],
+                               "failed": quest.jit_stats()[1],
+                               "compile_wait_s": round(jit_wait_s, 2) if args.warmup else None}},
             "gpu_launches": int(launches),
             "e2e": {"value": round(e2e, 1), "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h,

@@ -119,6 +119,22 @@ int qgpuPlanGate(int flatQubits, int rankLog2, int rank, int target,
 int qgpuPlanChunks(unsigned long long localLen, unsigned long long chunkAmps,
                    unsigned long long* chunkLen);
 
+/* Per-pass JIT of the fused tile pass: each distinct pass shape (op kinds,
+ * qubit positions, control masks; not the angles) is compiled once with
+ * NVRTC into straight-line code on background threads, and passes of that
+ * shape use it from then on (results are identical to the interpreter).
+ * mode 0 = off, 1 = background compiles (default; env QGPU_JIT=off|sync),
+ * 2 = compile before the first launch of a shape. qgpuJitWait blocks until
+ * every queued compile has finished; qgpuJitStats reports compiled kernels,
+ * failures and pending compiles. */
+void qgpuSetJit(int mode);
+int qgpuGetJit(void);
+void qgpuJitWait(void);
+void qgpuJitStats(unsigned long long* kernels, unsigned long long* failed, unsigned long long* pending);
+/* Host-only (no GPU): compile a sample pass program for sm_100a with NVRTC.
+ * Returns the cubin size, or -1 (message in log); *seconds = compile time. */
+int qgpuJitSelfTest(char* log, int len, double* seconds);
+
 /* Memory plan. The reference's node model, restated:
  * modeled peak bytes per rank of an n-qubit vector on 2^rankLog2 ranks for
  * strategy 0 = FullClone (2x), 1 = HalfExchange (1.5x), 2 = PerAmplitude

@@ -1096,4 +1096,25 @@ int qgpuPlanSwaps(int flatQubits, int rankLog2, unsigned long long chunkAmps, in
     });
 }
 
+// ------------------------------------------------------------ per-pass JIT
+
+void qgpuSetJit(int mode) {
+    guarded_void("qgpuSetJit", [&] {
+        if (mode < 0 || mode > 2) throw qgpu::DomainError("JIT mode must be 0 (off), 1 (background) or 2 (sync)");
+        qgpu::jit_set_mode(mode);
+    });
+}
+
+int qgpuGetJit(void) { return qgpu::jit_mode(); }
+
+void qgpuJitWait(void) {
+    guarded_void("qgpuJitWait", [&] { qgpu::jit_wait(); });
+}
+
+void qgpuJitStats(unsigned long long* kernels, unsigned long long* failed, unsigned long long* pending) {
+    qgpu::jit_stats(kernels, failed, pending);
+}
+
+int qgpuJitSelfTest(char* log, int len, double* seconds) { return qgpu::jit_selftest(log, len, seconds); }
+
 } // extern "C"

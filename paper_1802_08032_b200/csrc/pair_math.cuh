@@ -14,8 +14,10 @@
 
 #include "qgpu_device.h"
 
+#ifndef __CUDACC_RTC__
 #include <cuda_runtime.h>
 #include <cstdint>
+#endif
 
 namespace qgpu {
 

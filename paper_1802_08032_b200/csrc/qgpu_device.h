@@ -8,7 +8,16 @@
 // index j + 2^N k (register.hpp:47-50).
 #pragma once
 
+#ifdef __CUDACC_RTC__ // NVRTC (tile_jit.cpp): no host headers
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef unsigned long long uint64_t;
+typedef int int32_t;
+typedef long long int64_t;
+#else
 #include <cstdint>
+#endif
 
 namespace qgpu {
 
@@ -147,7 +156,13 @@ struct TileOp {
 };
 static_assert(sizeof(TileOp) == 80, "TileOp layout");
 
-constexpr uint64_t tile_hdr(uint32_t code, uint32_t flags, uint32_t outcome,
+#if defined(__CUDACC__) || defined(__CUDACC_RTC__)
+#define QGPU_HD __host__ __device__
+#else
+#define QGPU_HD
+#endif
+
+QGPU_HD constexpr uint64_t tile_hdr(uint32_t code, uint32_t flags, uint32_t outcome,
                             uint32_t q0k, uint32_t q0p, uint32_t q1k, uint32_t q1p,
                             uint32_t lane_cm, uint32_t reg_cm, uint32_t warp_cm) {
     return uint64_t(code & 63) | uint64_t(flags & 15) << 6 |

@@ -28,6 +28,15 @@ void launch_pass(double2* amps, const PassParams& params, cudaStream_t s);
 // per pass.
 void launch_tile_pass(double2* amps, const TileParams& params, cudaStream_t s);
 
+// Per-pass JIT (tile_jit.cpp): launches the compiled kernel for this pass
+// shape and returns true, or returns false (not compiled yet / JIT off).
+bool launch_tile_pass_jit(double2* amps, const TileParams& params, cudaStream_t s);
+void jit_wait();              // block until every queued compile finished
+void jit_set_mode(int mode);  // 0 off, 1 background compiles, 2 compile before first use
+int jit_mode();
+void jit_stats(unsigned long long* kernels, unsigned long long* failed, unsigned long long* pending);
+int jit_selftest(char* log, int len, double* seconds); // host only: cubin bytes or -1
+
 // One 2x2 gate over all pairs (i, i + 2^t) whose base holds cmask
 // (reference kernels.cpp:43-59). Used for states too small to tile and for
 // the unfused (one pass per gate) mode.

@@ -1,597 +1,34 @@
-// tile_pass.cu — the hot kernel: one HBM read + write of the state applies a
-// whole run of queued ops (gates, dephasing, collapse), in order.
-//
-// Structure (qgpu_device.h: TileParams / TilePhase / TileOp):
-//  * one persistent CTA per SM walks tiles of 2^12 amplitudes (qubits 0-4 plus
-//    7 higher qubits chosen per pass);
-//  * HBM <-> shared memory through TMA: warp 0 issues cp.async.bulk loads
-//    (completion on an mbarrier) and bulk stores at tile boundaries, three
-//    64 KiB stages deep, so the streaming overlaps the ops and no register
-//    holds data in flight;
-//  * the ops run in phases: every thread holds 8 amplitudes in registers
-//    spanning the phase's 3 register qubits (lanes span qubits 0-4, the 16
-//    warps the remaining 4 tile qubits). Pair ops on register
-//    qubits stay in registers, on lane qubits they use warp shuffles, diagonal
-//    gates and channels are elementwise anywhere; between phases the tile is
-//    re-laid out through shared memory.
-//
-// Code-generation notes (each measured with ncu on this kernel):
-//  * the op table is copied to shared memory once per launch — read from the
-//    kernel-parameter bank every op missed the constant cache;
-//  * an op's header and coefficients are loaded one op ahead (OpCtx), so their
-//    latency hides behind the previous op; the op index is warp-uniform, so
-//    the loads address through uniform registers;
-//  * the host resolves each op to one handler code (TileCode), and the build
-//    passes -jump-table-density=1 to NVVM: one brx.idx per op instead of a
-//    binary search tree of compares;
-//  * outer-qubit controls are evaluated once per tile (a ballot per 32 ops),
-//    not per op and phase;
-//  * handlers never branch per element on run-time values (selects only where
-//    lane / register controls need them) — per-element branches made ptxas
-//    copy the whole 64-register tile around them;
-//  * warp-uniform controls (on warp or outer qubits) skip the op outright.
-#include "pair_math.cuh"
+// tile_pass.cu — the ahead-of-time instantiation of the tile pass (the
+// interpreter over the op table; device code in tile_device.cuh) and its
+// launcher, which prefers a per-pass JIT kernel (tile_jit.cpp) once compiled.
+#include "tile_device.cuh"
+
 #include "qgpu_kernels.h"
 #include "runtime.h"
 
 #include <cstdio>
+#include <string>
 #include <cuda_runtime.h>
 
 namespace qgpu {
 
 namespace {
 
-template <int RB>
-using Regs = double2[1 << RB];
-
-// ------------------------------------------------------------ PTX helpers
-
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-    asm volatile(
-        "{\n"
-        ".reg .pred p;\n"
-        "WAIT%=:\n"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-        "@!p bra WAIT%=;\n"
-        "}\n" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_load(void* smem_dst, const void* gmem_src, uint32_t bytes,
-                                         uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-            smem_u32(smem_dst)),
-        "l"(gmem_src), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
-}
-
-__device__ __forceinline__ void tma_store(void* gmem_dst, const void* smem_src, uint32_t bytes) {
-    asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gmem_dst),
-                 "r"(smem_u32(smem_src)), "r"(bytes)
-                 : "memory");
-}
-
-__device__ __forceinline__ void tma_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-
-template <int N>
-__device__ __forceinline__ void tma_wait_read() {
-    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
-}
-
-__device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
-
-__device__ __forceinline__ void fence_proxy_async() {
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-}
-
-// ---------------------------------------------------------------- handlers
-//
-// Ping-pong: every handler reads the tile s and writes every element of the
-// tile d (a fresh register set), so the results of all switch arms land in
-// the same registers with no copies; the op loop alternates s and d. (An
-// in-place update leaves each pair's results in rotated registers, and ptxas
-// then copies the whole tile back at every loop iteration: measured 30 %
-// slower.) SEL variants apply a per-element predicate: register controls
-// `rcm` and lane controls (`tok`).
-
-__device__ __forceinline__ double2 diag_a(const double* c, double2 v) {
-    return make_double2(fma(c[0], v.x, -(c[1] * v.y)), fma(c[0], v.y, c[1] * v.x));
-}
-__device__ __forceinline__ double2 diag_d(const double* c, double2 v) {
-    return make_double2(fma(-c[7], v.y, c[6] * v.x), fma(c[7], v.x, c[6] * v.y));
-}
-
-__device__ __forceinline__ bool sel_on(int i, uint32_t rcm, bool tok) {
-    return tok && (static_cast<uint32_t>(i) & rcm) == rcm;
-}
-
-// 2x2 gate on register bit J (compile time).
-template <int RB, int J, int CLS, bool SEL>
-__device__ __forceinline__ void h_reg(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t rcm,
-                                      bool tok) {
-    if constexpr (J < RB) {
-#pragma unroll
-        for (int lo = 0; lo < (1 << RB); ++lo) {
-            constexpr int bit = 1 << J;
-            if (lo & bit) continue;
-            double2 l = s[lo], h = s[lo | bit];
-            pair_update<CLS>(l, h, c);
-            if constexpr (SEL) {
-                const bool on = sel_on(lo, rcm, tok);
-                d[lo] = on ? l : s[lo];
-                d[lo | bit] = on ? h : s[lo | bit];
-            } else {
-                d[lo] = l;
-                d[lo | bit] = h;
-            }
-        }
-    }
-}
-
-// 2x2 gate on lane bit b: the partner amplitude comes from lane ^ 2^b, and
-// each lane computes its own half (distributed.cpp:183-184:
-// own_lo ? lo_out(mine, theirs) : hi_out(theirs, mine)).
-template <int RB, int CLS, bool SEL>
-__device__ __forceinline__ void h_lane(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t b,
-                                       uint32_t rcm, bool tok, uint32_t lane) {
-    const uint32_t mask = 1u << b;
-    const bool own_lo = (lane & mask) == 0;
-    const double q0 = own_lo ? c[0] : c[4], q1 = own_lo ? c[1] : c[5];
-    const double q2 = own_lo ? c[2] : c[6], q3 = own_lo ? c[3] : c[7];
-#pragma unroll
-    for (int i = 0; i < (1 << RB); ++i) {
-        double2 th;
-        th.x = __shfl_xor_sync(0xffffffffu, s[i].x, mask);
-        th.y = __shfl_xor_sync(0xffffffffu, s[i].y, mask);
-        double2 r;
-        if constexpr (CLS == CLS_SWAP) {
-            r = th;
-        } else {
-            const double2 lo = own_lo ? s[i] : th;
-            const double2 hi = own_lo ? th : s[i];
-            r = row<CLS == CLS_REAL ? 0b1010 : 0>(q0, q1, q2, q3, lo, hi);
-        }
-        if constexpr (SEL)
-            d[i] = sel_on(i, rcm, tok) ? r : s[i];
-        else
-            d[i] = r;
-    }
-}
-
-// Diagonal gate, target on register bit J: a * v where the bit is 0, d * v
-// where it is 1 (rounding of the reference's low / high row). DO_A = false
-// leaves the low side alone (a == 1 exactly).
-template <int RB, int J, bool DO_A, bool SEL>
-__device__ __forceinline__ void h_diag_reg(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t rcm,
-                                           bool tok) {
-    if constexpr (J < RB) {
-#pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            const bool bit = (i >> J) & 1;
-            if (!bit && !DO_A) { // compile time
-                d[i] = s[i];
-                continue;
-            }
-            const double2 r = bit ? diag_d(c, s[i]) : diag_a(c, s[i]);
-            if constexpr (SEL)
-                d[i] = sel_on(i, rcm, tok) ? r : s[i];
-            else
-                d[i] = r;
-        }
-    }
-}
-
-// Diagonal gate whose target bit differs per lane: coefficients picked once
-// per thread; per element the operands swap:
-//   re = fma(P, X, Q * Y), im = fma(R, Y, S * X)
-//   bit 0: P = a_re, Q = -a_im, R = a_re, S = a_im, (X, Y) = (x, y)   (diag_a)
-//   bit 1: P = -d_im, Q = d_re, R = d_im, S = d_re, (X, Y) = (y, x)   (diag_d)
-template <int RB, bool SEL>
-__device__ __forceinline__ void h_diag_lane(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t bit,
-                                            uint32_t rcm, bool tok) {
-    const double P = bit ? -c[7] : c[0], Q = bit ? c[6] : -c[1];
-    const double R = bit ? c[7] : c[0], S = bit ? c[6] : c[1];
-#pragma unroll
-    for (int i = 0; i < (1 << RB); ++i) {
-        const double X = bit ? s[i].y : s[i].x, Y = bit ? s[i].x : s[i].y;
-        const double2 r = make_double2(fma(P, X, Q * Y), fma(R, Y, S * X));
-        if constexpr (SEL)
-            d[i] = sel_on(i, rcm, tok) ? r : s[i];
-        else
-            d[i] = r;
-    }
-}
-
-// Diagonal gate whose target bit is the same for the whole warp (a warp or
-// outer qubit): a warp-uniform branch picks the side.
-template <int RB, bool SEL>
-__device__ __forceinline__ void h_diag_uniform(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t bit,
-                                               uint32_t rcm, bool tok) {
-    if (bit) {
-#pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            const double2 r = diag_d(c, s[i]);
-            d[i] = SEL ? (sel_on(i, rcm, tok) ? r : s[i]) : r;
-        }
-    } else {
-#pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            const double2 r = diag_a(c, s[i]);
-            d[i] = SEL ? (sel_on(i, rcm, tok) ? r : s[i]) : r;
-        }
-    }
-}
-
-template <int RB>
-__device__ __forceinline__ void h_copy(const Regs<RB>& s, Regs<RB>& d) {
-#pragma unroll
-    for (int i = 0; i < (1 << RB); ++i) d[i] = s[i];
-}
-
-__device__ __forceinline__ uint32_t fixed_bit_of(uint32_t kind, uint32_t pos, uint32_t lane, uint32_t w,
-                                                 uint64_t gbase) {
-    return kind == TL_LANE   ? (lane >> pos) & 1u
-           : kind == TL_WARP ? (w >> pos) & 1u
-                             : static_cast<uint32_t>((gbase >> pos) & 1u);
-}
-
-// An op's header and coefficients, loaded one op ahead.
-struct OpCtx {
-    uint64_t h;
-    double c[8];
-};
-
-// Explicit shared-window addresses: through a generic pointer, ptxas
-// re-derived the CTA's shared window (S2R SR_CgaCtaId) at every op.
-__device__ __forceinline__ void load_ctx(OpCtx& x, uint32_t sops_addr, int o) {
-    const uint32_t a = sops_addr + static_cast<uint32_t>(o) * static_cast<uint32_t>(sizeof(TileOp));
-    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(x.h) : "r"(a));
-#pragma unroll
-    for (int k = 0; k < 8; k += 2)
-        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
-                     : "=d"(x.c[k]), "=d"(x.c[k + 1])
-                     : "r"(a + 16u + 8u * static_cast<uint32_t>(k)));
-}
-
-// Controls on outer qubits are uniform per tile: per tile, each warp
-// evaluates them once for all ops (one ballot per 32 ops) into a 64-bit mask
-// of the ops that run; the op loop walks the set bits. Controls on warp
-// qubits are not skipped but folded into the per-element predicate like lane
-// / register ones: a warp that skipped would idle at the next phase barrier
-// while its sub-partition ran the other warps alone.
-__device__ __forceinline__ uint64_t active_ops(const TileOp* ops, int nops, uint64_t gbase, uint32_t lane) {
-    bool a0 = false, a1 = false;
-    if (static_cast<int>(lane) < nops) {
-        const uint64_t m = ops[lane].outer_cmask;
-        a0 = (gbase & m) == m;
-    }
-    if (static_cast<int>(lane) + 32 < nops) {
-        const uint64_t m = ops[lane + 32].outer_cmask;
-        a1 = (gbase & m) == m;
-    }
-    return static_cast<uint64_t>(__ballot_sync(0xffffffffu, a0)) |
-           static_cast<uint64_t>(__ballot_sync(0xffffffffu, a1)) << 32;
-}
-
-__device__ __forceinline__ int lowest(uint64_t m) { return __ffsll(static_cast<long long>(m)) - 1; }
-
-// One op: s -> d. Header fields are decoded inside the arms that use them.
-template <int RB>
-__device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, const OpCtx& x, uint32_t lane,
-                                     uint32_t w, uint64_t gbase) {
-    const uint64_t h = x.h;
-    const uint32_t code = h & 63u;
-    const double* c = x.c;
-#define QGPU_Q0P ((h >> 13) & 63u)
-#define QGPU_RCM static_cast<uint32_t>((h >> 32) & 15u)
-#define QGPU_TOK                                                                          \
-    ((lane & static_cast<uint32_t>((h >> 27) & 31u)) == static_cast<uint32_t>((h >> 27) & 31u) && \
-     (w & static_cast<uint32_t>((h >> 36) & 15u)) == static_cast<uint32_t>((h >> 36) & 15u))
-    switch (code) {
-#define QGPU_REG(CODE, J, CLS)                                     \
-    case CODE: h_reg<RB, J, CLS, false>(s, d, c, 0, true); break;
-        QGPU_REG(TC_REG + 0, 0, CLS_GENERIC)
-        QGPU_REG(TC_REG + 1, 1, CLS_GENERIC)
-        QGPU_REG(TC_REG + 2, 2, CLS_GENERIC)
-        QGPU_REG(TC_REG + 3, 3, CLS_GENERIC)
-        QGPU_REG(TC_REG + 4, 0, CLS_REAL)
-        QGPU_REG(TC_REG + 5, 1, CLS_REAL)
-        QGPU_REG(TC_REG + 6, 2, CLS_REAL)
-        QGPU_REG(TC_REG + 7, 3, CLS_REAL)
-        QGPU_REG(TC_REG + 8, 0, CLS_RX)
-        QGPU_REG(TC_REG + 9, 1, CLS_RX)
-        QGPU_REG(TC_REG + 10, 2, CLS_RX)
-        QGPU_REG(TC_REG + 11, 3, CLS_RX)
-        QGPU_REG(TC_REG + 12, 0, CLS_SWAP)
-        QGPU_REG(TC_REG + 13, 1, CLS_SWAP)
-        QGPU_REG(TC_REG + 14, 2, CLS_SWAP)
-        QGPU_REG(TC_REG + 15, 3, CLS_SWAP)
-#undef QGPU_REG
-#define QGPU_REG_SEL(CODE, J, CLS)                                 \
-    case CODE: h_reg<RB, J, CLS, true>(s, d, c, QGPU_RCM, QGPU_TOK); break;
-        QGPU_REG_SEL(TC_REG_SEL + 0, 0, CLS_GENERIC)
-        QGPU_REG_SEL(TC_REG_SEL + 1, 1, CLS_GENERIC)
-        QGPU_REG_SEL(TC_REG_SEL + 2, 2, CLS_GENERIC)
-        QGPU_REG_SEL(TC_REG_SEL + 3, 3, CLS_GENERIC)
-        QGPU_REG_SEL(TC_REG_SEL + 4, 0, CLS_SWAP)
-        QGPU_REG_SEL(TC_REG_SEL + 5, 1, CLS_SWAP)
-        QGPU_REG_SEL(TC_REG_SEL + 6, 2, CLS_SWAP)
-        QGPU_REG_SEL(TC_REG_SEL + 7, 3, CLS_SWAP)
-#undef QGPU_REG_SEL
-    case TC_LANE_GENERIC: h_lane<RB, CLS_GENERIC, false>(s, d, c, QGPU_Q0P, 0, true, lane); break;
-    case TC_LANE_REAL: h_lane<RB, CLS_REAL, false>(s, d, c, QGPU_Q0P, 0, true, lane); break;
-    case TC_LANE_SWAP: h_lane<RB, CLS_SWAP, false>(s, d, c, QGPU_Q0P, 0, true, lane); break;
-    case TC_LANE_SEL_GENERIC: h_lane<RB, CLS_GENERIC, true>(s, d, c, QGPU_Q0P, QGPU_RCM, QGPU_TOK, lane); break;
-    case TC_LANE_SEL_SWAP: h_lane<RB, CLS_SWAP, true>(s, d, c, QGPU_Q0P, QGPU_RCM, QGPU_TOK, lane); break;
-#define QGPU_DIAG(CODE, J, DA)                                     \
-    case CODE: h_diag_reg<RB, J, DA, false>(s, d, c, 0, true); break;
-        QGPU_DIAG(TC_DIAG_REG + 0, 0, true)
-        QGPU_DIAG(TC_DIAG_REG + 1, 1, true)
-        QGPU_DIAG(TC_DIAG_REG + 2, 2, true)
-        QGPU_DIAG(TC_DIAG_REG + 3, 3, true)
-        QGPU_DIAG(TC_DIAG_REG_D + 0, 0, false)
-        QGPU_DIAG(TC_DIAG_REG_D + 1, 1, false)
-        QGPU_DIAG(TC_DIAG_REG_D + 2, 2, false)
-        QGPU_DIAG(TC_DIAG_REG_D + 3, 3, false)
-#undef QGPU_DIAG
-#define QGPU_DIAG_SEL(CODE, J, DA)                                 \
-    case CODE: h_diag_reg<RB, J, DA, true>(s, d, c, QGPU_RCM, QGPU_TOK); break;
-        QGPU_DIAG_SEL(TC_DIAG_REG_SEL + 0, 0, true)
-        QGPU_DIAG_SEL(TC_DIAG_REG_SEL + 1, 1, true)
-        QGPU_DIAG_SEL(TC_DIAG_REG_SEL + 2, 2, true)
-        QGPU_DIAG_SEL(TC_DIAG_REG_SEL + 3, 3, true)
-        QGPU_DIAG_SEL(TC_DIAG_REG_D_SEL + 0, 0, false)
-        QGPU_DIAG_SEL(TC_DIAG_REG_D_SEL + 1, 1, false)
-        QGPU_DIAG_SEL(TC_DIAG_REG_D_SEL + 2, 2, false)
-        QGPU_DIAG_SEL(TC_DIAG_REG_D_SEL + 3, 3, false)
-#undef QGPU_DIAG_SEL
-    case TC_DIAG_LANE: h_diag_lane<RB, false>(s, d, c, (lane >> QGPU_Q0P) & 1u, 0, true); break;
-    case TC_DIAG_LANE_SEL: h_diag_lane<RB, true>(s, d, c, (lane >> QGPU_Q0P) & 1u, QGPU_RCM, QGPU_TOK); break;
-    case TC_DIAG_UNIFORM:
-    case TC_DIAG_UNIFORM_SEL: {
-        const uint32_t flags = (h >> 6) & 15u;
-        const uint32_t bit = fixed_bit_of((h >> 11) & 3u, QGPU_Q0P, lane, w, gbase);
-        if (bit ? (flags & DF_D_ONE) : (flags & DF_A_ONE)) // identity side
-            h_copy<RB>(s, d);
-        else if (code == TC_DIAG_UNIFORM)
-            h_diag_uniform<RB, false>(s, d, c, bit, 0, true);
-        else
-            h_diag_uniform<RB, true>(s, d, c, bit, QGPU_RCM, QGPU_TOK);
-        break;
-    }
-    case TC_DEPHASE: { // density.cpp:56-59: scale where bit(q0) != bit(q1)
-        const uint32_t q0p = QGPU_Q0P;
-        const uint32_t q0k = (h >> 11) & 3u, q1k = (h >> 19) & 3u, q1p = (h >> 21) & 63u;
-        const uint32_t rm = (q0k == TL_REG ? 1u << q0p : 0u) ^ (q1k == TL_REG ? 1u << q1p : 0u);
-        const uint32_t f = (q0k == TL_REG ? 0u : fixed_bit_of(q0k, q0p, lane, w, gbase)) ^
-                           (q1k == TL_REG ? 0u : fixed_bit_of(q1k, q1p, lane, w, gbase));
-        const double sc = c[0];
-#pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            const bool on = (__popc(static_cast<uint32_t>(i) & rm) & 1u) ^ f;
-            const double k = on ? sc : 1.0; // x * 1.0 is exact
-            d[i] = make_double2(s[i].x * k, s[i].y * k);
-        }
-        break;
-    }
-    case TC_COLLAPSE: { // keep bit(q0) (and bit(q1)) == outcome, scaled
-        const uint32_t q0p = QGPU_Q0P;
-        const uint32_t flags = (h >> 6) & 15u;
-        const uint32_t q0k = (h >> 11) & 3u, q1k = (h >> 19) & 3u, q1p = (h >> 21) & 63u;
-        const uint32_t o = (h >> 10) & 1u;
-        const bool two = flags & 1;
-        const bool r0 = q0k == TL_REG, r1 = q1k == TL_REG;
-        const uint32_t f0 = r0 ? 0u : fixed_bit_of(q0k, q0p, lane, w, gbase);
-        const uint32_t f1 = r1 ? 0u : fixed_bit_of(q1k, q1p, lane, w, gbase);
-        const double sc = c[0];
-#pragma unroll
-        for (int i = 0; i < (1 << RB); ++i) {
-            const uint32_t b0 = r0 ? (static_cast<uint32_t>(i) >> q0p) & 1u : f0;
-            const uint32_t b1 = r1 ? (static_cast<uint32_t>(i) >> q1p) & 1u : f1;
-            const bool keep = b0 == o && (!two || b1 == o);
-            d[i] = make_double2(keep ? s[i].x * sc : 0.0, keep ? s[i].y * sc : 0.0);
-        }
-        break;
-    }
-    default: __builtin_unreachable(); // the host emits TileCode values only
-    }
-#undef QGPU_Q0P
-#undef QGPU_RCM
-#undef QGPU_TOK
-}
-
-// Global index of tile T's amplitude 0: T's bits deposited into the qubits
-// outside the tile. Linear in T, so a table per byte of T (built once per
-// launch) replaces the per-bit insertion loop.
-template <int RB, int WB>
-__device__ __forceinline__ uint64_t tile_gbase_slow(const TileParams& P, uint64_t T) {
-    uint64_t gb = T << kLaneQubits;
-#pragma unroll
-    for (int j = 0; j < RB + WB; ++j) gb = insert_zero_bit(gb, P.high_pos[j]);
-    return gb;
-}
-
-// All 2^WB warps apply the ops and share the TMA copies at tile boundaries
-// (one bulk copy per thread: a single issuing warp made the others wait at
-// the next phase barrier, 33 % of all stall samples). full[b]: stage b holds
-// a loaded tile (tx-count barrier). After the block barrier that ends tile t,
-// the threads bulk-store stage t % NBUF and refill the stage freed one tile
-// earlier with tile t - 1 + NBUF; each thread waited for its own part of that
-// stage's store to leave shared memory before the barrier, long after it was
-// issued, so the wait never stalls. No separate producer warp: 8 warps (2 per
-// SM sub-partition) may use 255 registers each, where a 9th warp would cap
-// them at 168.
 template <int RB, int WB, int NBUF>
 __global__ void __launch_bounds__(32 << WB, 1)
 k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
-    constexpr int R = 1 << RB;
-    constexpr int K = kLaneQubits + RB + WB;
-    constexpr int NSEG = 1 << (RB + WB);
-    constexpr uint32_t TILE_BYTES = sizeof(double2) << K;
-    extern __shared__ __align__(128) double2 smem[];
-    __shared__ TileOp sops[kMaxTileOps + 1]; // + 1: the prefetch may read one past
-    __shared__ uint64_t full[NBUF];
-    const uint32_t lane = threadIdx.x & 31u;
-    const uint32_t w = threadIdx.x >> 5;
-    const int nph = P.num_phases;
-    const bool any_outer = P.any_outer != 0;
-    constexpr int kGbaseChunks = (36 - K + 7) / 8; // tile indices of <= 36 local qubits
-    const uint64_t G = gridDim.x;
-    const uint64_t ntiles = P.num_tiles > blockIdx.x ? (P.num_tiles - blockIdx.x + G - 1) / G : 0;
-
-    __shared__ uint64_t gtab[kGbaseChunks][256];
-    auto tile_gbase = [&](uint64_t T) {
-        uint64_t g = 0;
-#pragma unroll
-        for (int k = 0; k < kGbaseChunks; ++k) g |= gtab[k][(T >> (8 * k)) & 255u];
-        return g;
-    };
-
-    // Each warp owns 8 whole 512-byte segments of the tile in the last phase
-    // (tile bits 0-4 are never warp bits, so a warp's amplitudes there are
-    // the segments with its own warp bits: P.fin_seg[w]). It stores them and
-    // refills their slots itself — lanes 0-7 one bulk copy each, lane 0
-    // posting the warp's 4 KiB on the stage's tx-count mbarrier (16
-    // arrivals per fill) — so no block barrier separates tiles.
-    constexpr uint32_t SEG_BYTES = 32u * sizeof(double2);
-    const uint32_t my_seg = lane < 8 ? P.fin_seg[w][lane] : 0;
-    auto load_mine = [&](uint64_t t) {
-        const int b = static_cast<int>(t % NBUF);
-        const uint64_t gb = tile_gbase(blockIdx.x + t * G);
-        double2* buf = smem + (static_cast<size_t>(b) << K);
-        if (lane < 8)
-            tma_load(buf + (my_seg << kLaneQubits), amps + gb + P.seg_off[my_seg], SEG_BYTES, &full[b]);
-        if (lane == 0) mbar_expect_tx(&full[b], 8 * SEG_BYTES);
-    };
-    auto store_mine = [&](uint64_t t) {
-        const int b = static_cast<int>(t % NBUF);
-        const uint64_t gb = tile_gbase(blockIdx.x + t * G);
-        double2* buf = smem + (static_cast<size_t>(b) << K);
-        if (lane < 8) {
-            tma_store(amps + gb + P.seg_off[my_seg], buf + (my_seg << kLaneQubits), SEG_BYTES);
-            tma_commit();
-        }
-    };
-
-    if (threadIdx.x == 0) {
-        for (int b = 0; b < NBUF; ++b) mbar_init(&full[b], 1u << WB);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
-    for (int k = threadIdx.x; k < kGbaseChunks * 256; k += blockDim.x)
-        gtab[k >> 8][k & 255] = tile_gbase_slow<RB, WB>(P, static_cast<uint64_t>(k & 255) << (8 * (k >> 8)));
-    __syncthreads();
-    for (uint64_t t = 0; t < NBUF && t < ntiles; ++t) load_mine(t);
-    const int nops = P.phases[nph - 1].op_end;
-    const uint32_t sops_addr = smem_u32(sops);
-    {
-        const uint64_t* src = reinterpret_cast<const uint64_t*>(P.ops);
-        uint64_t* dst = reinterpret_cast<uint64_t*>(sops);
-        constexpr int WORDS = sizeof(TileOp) / sizeof(uint64_t);
-        for (int k = threadIdx.x; k < (kMaxTileOps + 1) * WORDS; k += blockDim.x)
-            dst[k] = k < nops * WORDS ? src[k] : 0; // entry kMaxTileOps: the prefetch sentinel
-    }
-    __syncthreads();
-
-    for (uint64_t t = 0; t < ntiles; ++t) {
-        const int b = static_cast<int>(t % NBUF);
-        double2* buf = smem + (static_cast<size_t>(b) << K);
-        const uint64_t gbase = tile_gbase(blockIdx.x + t * G) + P.global_offset;
-        const uint64_t act = any_outer ? active_ops(sops, nops, gbase, lane) : ~uint64_t{0};
-        mbar_wait(&full[b], static_cast<uint32_t>((t / NBUF) & 1));
-        bool wrote = false, last_skipped = false; // (uniform per tile)
-        for (int ph = 0; ph < nph; ++ph) {
-            const TilePhase& Q = P.phases[ph];
-            const int end = Q.op_end;
-            uint64_t m = act & ((uint64_t{1} << end) - 1) &
-                         ~((uint64_t{1} << Q.op_begin) - 1);
-            if (m == 0) { // no op runs: the tile stays as it is in shared memory
-                last_skipped = ph == nph - 1;
-                continue;
-            }
-            // end < 64 always: kMaxTileOps entries plus the sentinel
-            if (wrote) { // the previous phase's writes are in (within the group)
-                const int c = Q.sync_bits;
-                if (c == 0)
-                    __syncthreads();
-                else if (c >= WB)
-                    __syncwarp();
-                else
-                    asm volatile("bar.sync %0, %1;" ::"r"(1 + (w >> (WB - c))), "r"(32 << (WB - c))
-                                 : "memory");
-            }
-            wrote = true;
-            const uint32_t wofs = Q.warp_off[w] + (lane & 7u) + ((lane >> 3) & 1u ? Q.lane_off[0] : 0u) +
-                                  ((lane >> 4) & 1u ? Q.lane_off[1] : 0u);
-            double2 a[R], b[R];
-#pragma unroll
-            for (int i = 0; i < R; ++i) a[i] = buf[wofs + Q.reg_off[i]];
-            // ops alternate a -> b, b -> a; the contexts alternate too, each
-            // loaded one op ahead. `run` has a bit per op that runs on this
-            // tile, plus a stop bit at the phase end (sops[end] is a valid
-            // entry: the next phase's first op or the zero sentinel).
-            const uint64_t runm = m | (uint64_t{1} << end);
-            // next op at or after `from`: one bit scan (runm has the stop bit)
-            auto next = [&](int from) { return lowest(runm & (~uint64_t{0} << from)); };
-            int o = next(Q.op_begin);
-            OpCtx ca, cb;
-            load_ctx(ca, sops_addr, o);
-            for (;;) {
-                const int on = next(o + 1);
-                load_ctx(cb, sops_addr, on);
-                step<RB>(a, b, ca, lane, w, gbase);
-                if (on >= end) {
-#pragma unroll
-                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = b[i];
-                    break;
-                }
-                o = next(on + 1);
-                load_ctx(ca, sops_addr, o);
-                step<RB>(b, a, cb, lane, w, gbase);
-                if (o >= end) {
-#pragma unroll
-                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = a[i];
-                    break;
-                }
-            }
-        }
-        // the warp's segments hold its own last-phase writes — unless the
-        // last phase was skipped on this tile after an earlier one wrote
-        // (rare: outer controls); then other warps wrote them
-        if (last_skipped && wrote) __syncthreads();
-        fence_proxy_async(); // generic-proxy writes -> visible to the bulk store
-        __syncwarp();
-        store_mine(t);
-        if (t >= 1 && t - 1 + NBUF < ntiles) {
-            if (lane < 8) tma_wait_read<1>(); // the store of tile t - 1 left the slot
-            load_mine(t - 1 + NBUF);
-        }
-    }
-    if (lane < 8) tma_wait_all();
+    tile_pass_body<RB, WB, NBUF, Interp>(amps, P);
 }
 
 } // namespace
 
 void launch_tile_pass(double2* amps, const TileParams& p, cudaStream_t s) {
+    if (launch_tile_pass_jit(amps, p, s)) { // straight-line kernel for this pass shape
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) throw DeviceError(std::string("jit tile pass launch: ") + cudaGetErrorString(e));
+        count_launch();
+        return;
+    }
     constexpr int NBUF = 3;
     auto kern = k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF>;
     constexpr size_t smem = NBUF * (sizeof(double2) << kTileQubits);

@@ -163,6 +163,11 @@ _SIGS = {
     "qgpuMaxQubits": (_I, [_ULL, _ULL, _I, _I, _I]),
     "qgpuDeviceBytesPerRank": (_ULL, [_I, _I, _ULL]),
     "qgpuDeviceMaxQubits": (_I, [_ULL, _I, _ULL, _I]),
+    "qgpuSetJit": (None, [_I]),
+    "qgpuGetJit": (_I, []),
+    "qgpuJitWait": (None, []),
+    "qgpuJitStats": (None, [_VP, _VP, _VP]),
+    "qgpuJitSelfTest": (_I, [ctypes.c_char_p, _I, ctypes.POINTER(ctypes.c_double)]),
     "qgpuProfileStart": (None, [QuESTEnv]),
     "qgpuProfileStop": (_I, [QuESTEnv, _VP, _VP, _I]),
 }
@@ -434,3 +439,29 @@ def plan_swaps(flat: int, rank_log2: int, ops, chunk_amps: int = 1 << 24):
     if n < 0:
         check()
     return [tuple(int(x) for x in out[3 * i:3 * i + 3]) for i in range(n)]
+
+
+def set_jit(mode: int):
+    """Per-pass JIT: 0 off, 1 background compiles (default), 2 compile before first use."""
+    call("qgpuSetJit", mode)
+
+
+def jit_wait():
+    call("qgpuJitWait")
+
+
+def jit_stats() -> tuple[int, int, int]:
+    """(compiled kernels, failed compiles, pending compiles)."""
+    import numpy as np
+
+    out = np.zeros(3, dtype=np.uint64)
+    lib().qgpuJitStats(out[0:].ctypes.data, out[1:].ctypes.data, out[2:].ctypes.data)
+    return int(out[0]), int(out[1]), int(out[2])
+
+
+def jit_selftest() -> tuple[int, str, float]:
+    """Host-only NVRTC compile of a sample pass: (cubin bytes or -1, log, seconds)."""
+    buf = ctypes.create_string_buffer(1 << 16)
+    sec = ctypes.c_double()
+    n = lib().qgpuJitSelfTest(buf, len(buf), ctypes.byref(sec))
+    return n, buf.value.decode(errors="replace"), sec.value

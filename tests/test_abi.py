@@ -83,3 +83,11 @@ def test_planner_rejects_bad_input():
 def test_chunk_plan():
     assert quest.plan_chunks(1 << 20, 1 << 16) == (16, 1 << 16)
     assert quest.plan_chunks(1 << 10, 1 << 16) == (1, 1 << 10)
+
+
+def test_jit_compiles_sample_pass_for_sm100a():
+    """The per-pass JIT's generated code (register, lane, diagonal, controlled
+    and channel handlers over two phases) compiles with NVRTC for sm_100a —
+    host only, no GPU."""
+    n, log, sec = quest.jit_selftest()
+    assert n > 0, log

@@ -406,3 +406,27 @@ def test_14q_density_config_c4_against_reference(env):
         assert_parity(q.state(), want)
     finally:
         q.destroy()
+
+
+@pytest.fixture
+def jit_sync():
+    quest.set_jit(2)  # compile every pass shape before its first launch
+    yield
+    quest.set_jit(1)
+
+
+@pytest.mark.parametrize("n", [12, 14, 17])
+def test_jit_passes_bit_identical(env, jit_sync, n):
+    """Per-pass JIT kernels (straight-line handler calls) give the oracle's
+    amplitudes bit for bit: random gates with controls anywhere (outer ones
+    skip per tile), a layered circuit, and a noisy density matrix."""
+    before = quest.jit_stats()[0]
+    c = random_gate_circuit(n, 150, seed=300 + n, max_controls=3)
+    assert_parity(run_product(env, c), oracle_run(c))
+    lc = C.layered_random_circuit(n, 6, 31 + n)
+    assert_parity(run_product(env, lc), oracle_run(lc))
+    if n == 12:
+        d = C.layered_random_circuit(6, 3, 8, noise_pmax=0.1)
+        assert_parity(run_product(env, d, density=True), oracle_run(d, density=True))
+    assert quest.jit_stats()[0] > before  # kernels were compiled and used
+    assert quest.jit_stats()[1] == 0
