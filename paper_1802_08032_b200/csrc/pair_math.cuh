@@ -57,7 +57,8 @@ __device__ __forceinline__ double2 row(double q0, double q1, double q2, double q
         im = fma(q2, hi.y, im);
     }
     if constexpr (n3) {
-        re = fma(-q3, hi.y, re);
+        re = fma(q3, -hi.y, re); // = fma(-q3, y1, re) exactly; the negation stays on
+                                 // the register operand so q3 can be a constant-bank one
         im = fma(q3, hi.x, im);
     }
     return make_double2(re, im);

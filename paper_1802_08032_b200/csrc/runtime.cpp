@@ -231,6 +231,14 @@ bool QuregImpl::use_tile() const { return local_qubits >= kTileQubits; }
 // kPhaseRegBits register qubits. Diagonal gates, dephasing and collapse act
 // elementwise and fit anywhere.
 
+// Phases per pass: QGPU_TILE_PHASES / Env::tile_phases if set, else 3 when
+// the per-pass JIT is on and 2 for the interpreter (profiles/: a transition
+// costs ~3 interpreted ops but only ~5 straight-line ones).
+int QuregImpl::max_phases() const {
+    if (env->tile_phases > 0) return env->tile_phases;
+    return jit_mode() != 0 ? 3 : 2;
+}
+
 bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
     if (phases.empty()) phases.push_back(PhaseState{});
     if (pair && op.q0 >= kFixedLaneBits) {
@@ -246,7 +254,7 @@ bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
             if (!in_tile && static_cast<int>(tile_high.size()) >= env->tile_targets) return false;
             // a phase holds kPhaseRegBits register qubits
             if (!in_phase && static_cast<int>(ph.regs.size()) >= kPhaseRegBits) {
-                if (static_cast<int>(phases.size()) >= env->tile_phases) return false;
+                if (static_cast<int>(phases.size()) >= max_phases()) return false;
                 PhaseState next;
                 next.op_begin = static_cast<int>(pending.size());
                 phases.push_back(next);

@@ -55,7 +55,7 @@ struct Env {
     // dynamic-programming pass planner over a calibrated cost model predicted
     // no further gain.
     int tile_targets = kTileHigh; // distinct pair targets above qubit 4 per pass
-    int tile_phases = 2;          // register phases per pass
+    int tile_phases = 0;          // register phases per pass (0: by JIT mode)
     uint64_t chunk_amps = uint64_t{1} << 24;
     // global<->local qubit swaps instead of per-gate exchanges (swap_plan.h);
     // qgpuSetQubitSwaps turns them off (the reference's exchange per gate)
@@ -180,6 +180,7 @@ struct QuregImpl {
     int pass_H() const;
     bool use_tile() const;
     bool place_tile(const FlatOp& op, bool pair);
+    int max_phases() const;
     void launch_tile();
     void run_simple(const FlatOp& op);
     void launch_fused();

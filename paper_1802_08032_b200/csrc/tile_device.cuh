@@ -117,7 +117,8 @@ __device__ __forceinline__ double2 diag_a(const double* c, double2 v) {
     return make_double2(fma(c[0], v.x, -(c[1] * v.y)), fma(c[0], v.y, c[1] * v.x));
 }
 __device__ __forceinline__ double2 diag_d(const double* c, double2 v) {
-    return make_double2(fma(-c[7], v.y, c[6] * v.x), fma(c[7], v.x, c[6] * v.y));
+    // fma(-d_im, y, ...) with the (exact) negation on the register operand
+    return make_double2(fma(c[7], -v.y, c[6] * v.x), fma(c[7], v.x, c[6] * v.y));
 }
 
 __device__ __forceinline__ bool sel_on(int i, uint32_t rcm, bool tok) {
@@ -202,18 +203,22 @@ __device__ __forceinline__ void h_diag_reg(const Regs<RB>& s, Regs<RB>& d, const
 
 // Diagonal gate whose target bit differs per lane: coefficients picked once
 // per thread; per element the operands swap:
-//   re = fma(P, X, Q * Y), im = fma(R, Y, S * X)
-//   bit 0: P = a_re, Q = -a_im, R = a_re, S = a_im, (X, Y) = (x, y)   (diag_a)
-//   bit 1: P = -d_im, Q = d_re, R = d_im, S = d_re, (X, Y) = (y, x)   (diag_d)
+//   re = fma(P, X1, Q * Y1), im = fma(R, Y2, S * X2)
+//   bit 0: P = R = a_re, Q = S = a_im, (X1, Y1) = (x, -y), (X2, Y2) = (x, y)  (diag_a)
+//   bit 1: P = R = d_im, Q = S = d_re, (X1, Y1) = (-y, x), (X2, Y2) = (y, x)  (diag_d)
+// (negations are exact, and sit on register operands: see diag_d)
 template <int RB, bool SEL>
 __device__ __forceinline__ void h_diag_lane(const Regs<RB>& s, Regs<RB>& d, const double* c, uint32_t bit,
                                             uint32_t rcm, bool tok) {
-    const double P = bit ? -c[7] : c[0], Q = bit ? c[6] : -c[1];
+    // signs moved from the coefficients onto the (exact) operand negations
+    const double P = bit ? c[7] : c[0], Q = bit ? c[6] : c[1];
     const double R = bit ? c[7] : c[0], S = bit ? c[6] : c[1];
 #pragma unroll
     for (int i = 0; i < (1 << RB); ++i) {
-        const double X = bit ? s[i].y : s[i].x, Y = bit ? s[i].x : s[i].y;
-        const double2 r = make_double2(fma(P, X, Q * Y), fma(R, Y, S * X));
+        const double x = s[i].x, y = s[i].y;
+        const double X1 = bit ? -y : x, Y1 = bit ? x : -y; // re = fma(P, X1, Q * Y1)
+        const double X2 = bit ? y : x, Y2 = bit ? x : y;   // im = fma(R, Y2, S * X2)
+        const double2 r = make_double2(fma(P, X1, Q * Y1), fma(R, Y2, S * X2));
         if constexpr (SEL)
             d[i] = sel_on(i, rcm, tok) ? r : s[i];
         else
@@ -265,6 +270,18 @@ struct OpCtx {
 __device__ __forceinline__ void load_ctx(OpCtx& x, uint32_t sops_addr, int o) {
     const uint32_t a = sops_addr + static_cast<uint32_t>(o) * static_cast<uint32_t>(sizeof(TileOp));
     asm volatile("ld.shared.u64 %0, [%1];" : "=l"(x.h) : "r"(a));
+#pragma unroll
+    for (int k = 0; k < 8; k += 2)
+        asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
+                     : "=d"(x.c[k]), "=d"(x.c[k + 1])
+                     : "r"(a + 16u + 8u * static_cast<uint32_t>(k)));
+}
+
+// Coefficients only (a JIT program's headers are literals). Volatile, so
+// NVVM cannot hoist them out of the tile loop: hoisting all of a pass's
+// coefficients into registers spilled (measured: 128 regs + 576 B stack).
+__device__ __forceinline__ void load_coef(OpCtx& x, uint32_t sops_addr, int o) {
+    const uint32_t a = sops_addr + static_cast<uint32_t>(o) * static_cast<uint32_t>(sizeof(TileOp));
 #pragma unroll
     for (int k = 0; k < 8; k += 2)
         asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];"
@@ -551,7 +568,7 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
                 }
             } else {
                 // a generated straight-line program (tile_jit.cpp)
-                in_a = Prog::template run<RB>(ph, m, a, b, P, lane, w, gbase);
+                in_a = Prog::template run<RB>(ph, m, a, b, P, lane, w, gbase, sops_addr);
             }
             if (in_a) {
 #pragma unroll

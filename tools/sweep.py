@@ -34,6 +34,10 @@ for kind in a.kinds.split(","):
         C.apply_circuit(q, c)
         q.flush()
         env.sync()
+        quest.jit_wait()  # per-pass JIT: compile this shape before timing
+        C.apply_circuit(q, c)
+        q.flush()
+        env.sync()
         env.profile_start()
         for _ in range(a.reps):
             C.apply_circuit(q, c)
