@@ -280,6 +280,9 @@ def run_ours(args):
     achieved = per_launch_bytes / (float(pass_ms.mean()) / 1e3) / 1e9 if pass_ms.size else None
     share = float(pass_ms.sum()) / float(ms_launch.sum()) if ms_launch.size else None
 
+    # sanity: the timed steps kept the state normalised
+    norm_error = abs(q.calcTotalProb() - 1.0)
+
     # e2e through the C-ABI from the host: init + gates + readback, wall clock
     e2e_vals = []
     for _ in range(max(1, min(args.steps, 3))):
@@ -339,6 +342,7 @@ def run_ours(args):
                          "avg_launch_ms": round(float(pass_ms.mean()), 4) if pass_ms.size else None,
                          "launches": int(pass_ms.size), "share_of_step": round(share, 4) if share else None},
             "clocks": clocks.summary(),
+            "check": {"norm_error_after_timed_steps": norm_error},
             "cpu_baseline": cpu,
         }
         if exch_ms.size or swap_ms.size:

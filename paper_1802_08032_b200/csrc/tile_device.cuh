@@ -471,12 +471,16 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
     // arrivals per fill) — so no block barrier separates tiles.
     constexpr uint32_t SEG_BYTES = 32u * sizeof(double2);
     const uint32_t my_seg = lane < 8 ? P.fin_seg[w][lane] : 0;
+    // per-lane offsets of its segment, read once (a per-tile indexed
+    // parameter load stalled the copy issue loop)
+    const uint64_t my_goff = P.seg_off[my_seg];
+    const uint32_t my_soff = my_seg << kLaneQubits;
     auto load_mine = [&](uint64_t t) {
         const int b = static_cast<int>(t % NBUF);
         const uint64_t gb = tile_gbase(blockIdx.x + t * G);
         double2* buf = smem + (static_cast<size_t>(b) << K);
         if (lane < 8)
-            tma_load(buf + (my_seg << kLaneQubits), amps + gb + P.seg_off[my_seg], SEG_BYTES, &full[b]);
+            tma_load(buf + my_soff, amps + gb + my_goff, SEG_BYTES, &full[b]);
         if (lane == 0) mbar_expect_tx(&full[b], 8 * SEG_BYTES);
     };
     auto store_mine = [&](uint64_t t) {
@@ -484,7 +488,7 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
         const uint64_t gb = tile_gbase(blockIdx.x + t * G);
         double2* buf = smem + (static_cast<size_t>(b) << K);
         if (lane < 8) {
-            tma_store(amps + gb + P.seg_off[my_seg], buf + (my_seg << kLaneQubits), SEG_BYTES);
+            tma_store(amps + gb + my_goff, buf + my_soff, SEG_BYTES);
             tma_commit();
         }
     };
@@ -515,6 +519,7 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
         const uint64_t act = any_outer ? active_ops(sops, nops, gbase, lane) : ~uint64_t{0};
         mbar_wait(&full[b], static_cast<uint32_t>((t / NBUF) & 1));
         bool wrote = false, last_skipped = false; // (uniform per tile)
+        int prev_ph = -1;                         // the last phase executed
         for (int ph = 0; ph < nph; ++ph) {
             const TilePhase& Q = P.phases[ph];
             const int end = Q.op_end;
@@ -526,7 +531,10 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
             }
             // end < 64 always: kMaxTileOps entries plus the sentinel
             if (wrote) { // the previous phase's writes are in (within the group)
-                const int c = Q.sync_bits;
+                // group barriers hold for the transition ph - 1 -> ph only; if
+                // outer controls skipped phase ph - 1 on this tile, the data
+                // comes from an earlier layout: sync the whole CTA
+                const int c = prev_ph == ph - 1 ? Q.sync_bits : 0;
                 if (c == 0)
                     __syncthreads();
                 else if (c >= WB)
@@ -536,13 +544,14 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
                                  : "memory");
             }
             wrote = true;
-            const uint32_t wofs = Q.warp_off[w] + (lane & 7u) + ((lane >> 3) & 1u ? Q.lane_off[0] : 0u) +
-                                  ((lane >> 4) & 1u ? Q.lane_off[1] : 0u);
-            double2 a[R], b[R];
-#pragma unroll
-            for (int i = 0; i < R; ++i) a[i] = buf[wofs + Q.reg_off[i]];
-            bool in_a = true; // the phase's result is in a (else b)
+            prev_ph = ph;
             if constexpr (Prog::kInterp) {
+                const uint32_t wofs = Q.warp_off[w] + (lane & 7u) + ((lane >> 3) & 1u ? Q.lane_off[0] : 0u) +
+                                      ((lane >> 4) & 1u ? Q.lane_off[1] : 0u);
+                double2 a[R], b[R];
+#pragma unroll
+                for (int i = 0; i < R; ++i) a[i] = buf[wofs + Q.reg_off[i]];
+                bool in_a = true; // the phase's result is in a (else b)
                 // ops alternate a -> b, b -> a; the contexts alternate too,
                 // each loaded one op ahead. `runm` has a bit per op that runs
                 // on this tile, plus a stop bit at the phase end (sops[end] is
@@ -566,16 +575,17 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
                     step<RB>(b, a, cb, lane, w, gbase);
                     if (o >= end) break;
                 }
-            } else {
-                // a generated straight-line program (tile_jit.cpp)
-                in_a = Prog::template run<RB>(ph, m, a, b, P, lane, w, gbase, sops_addr);
-            }
-            if (in_a) {
+                if (in_a) {
 #pragma unroll
-                for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = a[i];
-            } else {
+                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = a[i];
+                } else {
 #pragma unroll
-                for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = b[i];
+                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = b[i];
+                }
+            } else {
+                // a generated straight-line program (tile_jit.cpp): the
+                // phase's layout offsets and op sequence are literals
+                Prog::template phase<RB>(ph, m, buf, P, lane, w, gbase, sops_addr);
             }
         }
         // the warp's segments hold its own last-phase writes — unless the

@@ -430,3 +430,27 @@ def test_jit_passes_bit_identical(env, jit_sync, n):
         assert_parity(run_product(env, d, density=True), oracle_run(d, density=True))
     assert quest.jit_stats()[0] > before  # kernels were compiled and used
     assert quest.jit_stats()[1] == 0
+
+
+@pytest.mark.parametrize("phases", ["3", "8"])
+@pytest.mark.parametrize("n", [20, 22])
+def test_jit_equals_interpreter_multi_phase(monkeypatch, n, phases):
+    """Bigger registers with multi-phase passes: tiles where outer controls
+    skip a middle phase must resync the whole CTA (regression: a group
+    barrier computed for the skipped transition raced). JIT (sync) and the
+    interpreter agree bit for bit, and match the oracle at n = 20."""
+    monkeypatch.setenv("QGPU_TILE_PHASES", phases)
+    e = quest.Env()
+    try:
+        c = C.layered_random_circuit(n, 4, 12345)
+        out = {}
+        for mode in (0, 2):
+            quest.set_jit(mode)
+            out[mode] = run_product(e, c)
+        quest.set_jit(1)
+        assert np.array_equal(out[0], out[2])
+        if n == 20:
+            assert_parity(out[2], oracle_run(c))
+    finally:
+        quest.set_jit(1)
+        e.destroy()
