@@ -58,7 +58,8 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--fusion", type=int, default=0, help="0 fused, 1 pass per op, 2 simple kernels")
     p.add_argument("--reg-qubits", type=int, default=0)
-    p.add_argument("--jit", type=int, default=1, help="per-pass JIT: 0 off, 1 on (background compiles)")
+    p.add_argument("--jit", type=int, default=None,
+                   help="per-pass JIT: 0 off, 1 on (default; env QGPU_JIT=off|sync also applies)")
     return p.parse_args()
 
 
@@ -213,7 +214,8 @@ def run_ours(args):
         env = quest.Env()
     if args.fusion or args.reg_qubits:
         env.set_fusion(args.fusion, 0, args.reg_qubits)
-    quest.set_jit(args.jit)
+    if args.jit is not None:
+        quest.set_jit(args.jit)
     jit_wait_s = 0.0
     k = int(math.log2(world))
     n = args.local_qubits + k
