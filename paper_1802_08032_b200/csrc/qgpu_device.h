@@ -191,8 +191,10 @@ struct TileParams {
     uint64_t num_tiles;
     uint64_t global_offset;
     int32_t num_phases;
-    int32_t seg_run;                       // high_pos[0..seg_run) = 5, 6, ...: contiguous
-    int32_t high_pos[kTileHigh];           // ascending global qubits of tile bits 5..
+    int32_t seg_run;                       // (unused: pre-per-warp copies)
+    int32_t fin_run;                       // a warp's segments come in HBM runs of 2^fin_run
+    int32_t high_pos[kTileHigh];           // global qubits of tile bits 5.. (any order)
+    int32_t high_sorted[kTileHigh];        // the same qubits, ascending
     int32_t any_outer;                     // some op has controls outside the tile
     uint64_t seg_off[1 << kTileHigh];      // global offset of tile segment s
     // the 8 segments warp w owns in the last phase (its warp bits fixed)

@@ -519,6 +519,46 @@ void QuregImpl::launch_tile() {
             ++c;
         sync_bits[p] = c;
     }
+    // Renumber the high tile bits so the last phase's non-warp high bits sit
+    // at tile bits 5..7 in ascending qubit order: each warp's 8 last-phase
+    // segments are then contiguous in shared memory, and whenever those
+    // qubits are 5, 6, 7 they are contiguous in HBM too, so the warp moves
+    // them in fewer, larger bulk copies (P.fin_run). Only names change: the
+    // layouts above are remapped, not recomputed.
+    {
+        const std::vector<int>& wl = WBv[nph - 1];
+        std::vector<int> order; // new tile bit 5 + k := old tile bit order[k]
+        for (int t = kLaneQubits; t < kTileQubits; ++t)
+            if (!has(wl, t)) order.push_back(t);
+        for (int t = kLaneQubits; t < kTileQubits; ++t)
+            if (has(wl, t)) order.push_back(t);
+        std::vector<int> remap(kTileQubits);
+        for (int t = 0; t < kLaneQubits; ++t) remap[t] = t;
+        std::vector<int> nh(kTileHigh);
+        for (int k = 0; k < kTileHigh; ++k) {
+            remap[order[k]] = kLaneQubits + k;
+            nh[k] = high[order[k] - kLaneQubits];
+        }
+        high = nh;
+        for (size_t p = 0; p < nph; ++p)
+            for (auto* v : {&RB[p], &LB[p], &WBv[p]})
+                for (int& t : *v) t = remap[t];
+        for (int j = 0; j < kTileHigh; ++j) P.high_pos[j] = high[j];
+        {
+            std::vector<int> hs = high;
+            std::sort(hs.begin(), hs.end());
+            for (int j = 0; j < kTileHigh; ++j) P.high_sorted[j] = hs[j];
+        }
+        for (int sg = 0; sg < (1 << kTileHigh); ++sg) {
+            uint64_t off = 0;
+            for (int j = 0; j < kTileHigh; ++j)
+                if ((sg >> j) & 1) off |= uint64_t{1} << high[j];
+            P.seg_off[sg] = off;
+        }
+        int run = 0; // runs of 2^run segments contiguous in HBM
+        while (run < kTileHigh - kTileWarpBits && high[run] == kLaneQubits + run) ++run;
+        P.fin_run = run;
+    }
     for (size_t p = 0; p < phases.size(); ++p) {
         TilePhase& Q = P.phases[p];
         const std::vector<int>& rb = RB[p];

@@ -420,7 +420,7 @@ template <int RB, int WB>
 __device__ __forceinline__ uint64_t tile_gbase_slow(const TileParams& P, uint64_t T) {
     uint64_t gb = T << kLaneQubits;
 #pragma unroll
-    for (int j = 0; j < RB + WB; ++j) gb = insert_zero_bit(gb, P.high_pos[j]);
+    for (int j = 0; j < RB + WB; ++j) gb = insert_zero_bit(gb, P.high_sorted[j]); // ascending
     return gb;
 }
 
@@ -470,29 +470,31 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
     // posting the warp's 4 KiB on the stage's tx-count mbarrier (16
     // arrivals per fill) — so no block barrier separates tiles.
     constexpr uint32_t SEG_BYTES = 32u * sizeof(double2);
-    const uint32_t my_seg = lane < 8 ? P.fin_seg[w][lane] : 0;
-    // per-lane offsets of its segment, read once (a per-tile indexed
-    // parameter load stalled the copy issue loop)
-    const uint64_t my_goff = P.seg_off[my_seg];
-    const uint32_t my_soff = my_seg << kLaneQubits;
+    // runs of 2^fin_run segments are contiguous in HBM (and, by the host's
+    // tile-bit order, in shared memory): lanes 0 .. (8 >> fin_run) - 1 move
+    // one run each
+    const int frun = P.fin_run;
+    const uint32_t ncopy = 8u >> frun;
+    const uint32_t run_bytes = SEG_BYTES << frun;
+    const uint32_t my_rseg = lane < ncopy ? P.fin_seg[w][lane << frun] : 0;
+    const uint64_t my_goff = P.seg_off[my_rseg];
+    const uint32_t my_soff = my_rseg << kLaneQubits;
     auto load_mine = [&](uint64_t t) {
         const int b = static_cast<int>(t % NBUF);
         const uint64_t gb = tile_gbase(blockIdx.x + t * G);
         double2* buf = smem + (static_cast<size_t>(b) << K);
-        if (lane < 8)
-            tma_load(buf + my_soff, amps + gb + my_goff, SEG_BYTES, &full[b]);
+        if (lane < ncopy) tma_load(buf + my_soff, amps + gb + my_goff, run_bytes, &full[b]);
         if (lane == 0) mbar_expect_tx(&full[b], 8 * SEG_BYTES);
     };
     auto store_mine = [&](uint64_t t) {
         const int b = static_cast<int>(t % NBUF);
         const uint64_t gb = tile_gbase(blockIdx.x + t * G);
         double2* buf = smem + (static_cast<size_t>(b) << K);
-        if (lane < 8) {
-            tma_store(amps + gb + my_goff, buf + my_soff, SEG_BYTES);
+        if (lane < ncopy) {
+            tma_store(amps + gb + my_goff, buf + my_soff, run_bytes);
             tma_commit();
         }
     };
-
     constexpr uint32_t kCopyLanes = 8; // lanes 0-7: one segment each (a
     // lane-0 unrolled issue with uniform addresses measured 5 % slower)
     if (threadIdx.x == 0) {
