@@ -48,12 +48,11 @@ struct Env {
     int reg_qubits = 4;
     // tile-pass shape limits (scheduler tuning; QGPU_TILE_TARGETS /
     // QGPU_TILE_PHASES override them at Env creation). A phase transition
-    // (a shared-memory round trip of the whole tile plus a block barrier)
-    // costs about three register ops, and a fresh pass is free while the pass
-    // stays HBM-bound: measured on the 30-qubit layered circuit, at most two
-    // phases per pass is fastest (profiles/r1_scheduler_knobs.md), and a
-    // dynamic-programming pass planner over a calibrated cost model predicted
-    // no further gain.
+    // (a shared-memory round trip of the whole tile plus a barrier) costs
+    // about three interpreted ops or five JIT ops, and a fresh pass is free
+    // while the pass stays HBM-bound: measured on the 30-qubit layered
+    // circuit, at most two phases per pass is fastest for the interpreter and
+    // three under the JIT (profiles/r1_scheduler_knobs.md; max_phases()).
     int tile_targets = kTileHigh; // distinct pair targets above qubit 4 per pass
     int tile_phases = 0;          // register phases per pass (0: by JIT mode)
     uint64_t chunk_amps = uint64_t{1} << 24;
