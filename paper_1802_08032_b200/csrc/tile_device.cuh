@@ -474,7 +474,8 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
     // tile-bit order, in shared memory): lanes 0 .. (8 >> fin_run) - 1 move
     // one run each
     const int frun = P.fin_run;
-    const uint32_t ncopy = 8u >> frun;
+    constexpr uint32_t SEGS = 1u << RB; // segments a warp owns in the last phase
+    const uint32_t ncopy = SEGS >> frun;
     const uint32_t run_bytes = SEG_BYTES << frun;
     const uint32_t my_rseg = lane < ncopy ? P.fin_seg[w][lane << frun] : 0;
     const uint64_t my_goff = P.seg_off[my_rseg];
@@ -484,7 +485,7 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
         const uint64_t gb = tile_gbase(blockIdx.x + t * G);
         double2* buf = smem + (static_cast<size_t>(b) << K);
         if (lane < ncopy) tma_load(buf + my_soff, amps + gb + my_goff, run_bytes, &full[b]);
-        if (lane == 0) mbar_expect_tx(&full[b], 8 * SEG_BYTES);
+        if (lane == 0) mbar_expect_tx(&full[b], SEGS * SEG_BYTES);
     };
     auto store_mine = [&](uint64_t t) {
         const int b = static_cast<int>(t % NBUF);
@@ -495,7 +496,7 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
             tma_commit();
         }
     };
-    constexpr uint32_t kCopyLanes = 8; // lanes 0-7: one segment each (a
+    constexpr uint32_t kCopyLanes = SEGS; // one segment (run) per lane (a
     // lane-0 unrolled issue with uniform addresses measured 5 % slower)
     if (threadIdx.x == 0) {
         for (int b = 0; b < NBUF; ++b) mbar_init(&full[b], 1u << WB);
