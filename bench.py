@@ -285,6 +285,32 @@ def run_ours(args):
     # sanity: the timed steps kept the state normalised
     norm_error = abs(q.calcTotalProb() - 1.0)
 
+    # the same tile kernel run one gate per pass (fusion mode 1): the
+    # streaming roofline of a single-gate pass, the north star's "gate pass"
+    # (BASELINE.json), on the first 24 gates of the circuit
+    single = None
+    if args.fusion == 0:
+        sub = C.Circuit(n, circuit.depth, circuit.ops[:24])
+        env.set_fusion(1, 0, 0)
+        C.apply_circuit(q, sub)
+        q.flush()
+        quest.jit_wait()
+        C.apply_circuit(q, sub)
+        q.flush()
+        env.sync()
+        env.profile_start()
+        C.apply_circuit(q, sub)
+        q.flush()
+        env.sync()
+        ms1, k1 = env.profile_stop()
+        env.set_fusion(0, 0, 0)
+        p1 = ms1[k1 == 0]
+        if p1.size:
+            gbs = 2.0 * 16.0 * (2.0 ** args.local_qubits) / (float(p1.mean()) / 1e3) / 1e9
+            single = {"gates": int(p1.size), "avg_pass_ms": round(float(p1.mean()), 4),
+                      "achieved_GBps": round(gbs, 1), "frac": round(gbs / peaks()[0]["hbm_gbs"], 4),
+                      "what": "one gate per tile pass (fusion mode 1), same kernel, same bytes per pass"}
+
     # e2e through the C-ABI from the host: init + gates + readback, wall clock
     e2e_vals = []
     for _ in range(max(1, min(args.steps, 3))):
@@ -345,6 +371,7 @@ def run_ours(args):
                          "launches": int(pass_ms.size), "share_of_step": round(share, 4) if share else None},
             "clocks": clocks.summary(),
             "check": {"norm_error_after_timed_steps": norm_error},
+            "single_gate_pass": single,
             "cpu_baseline": cpu,
         }
         if exch_ms.size or swap_ms.size:
