@@ -191,7 +191,6 @@ struct TileParams {
     uint64_t num_tiles;
     uint64_t global_offset;
     int32_t num_phases;
-    int32_t seg_run;                       // (unused: pre-per-warp copies)
     int32_t fin_run;                       // a warp's segments come in HBM runs of 2^fin_run
     int32_t high_pos[kTileHigh];           // global qubits of tile bits 5.. (any order)
     int32_t high_sorted[kTileHigh];        // the same qubits, ascending

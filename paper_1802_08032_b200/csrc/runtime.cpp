@@ -403,14 +403,12 @@ void record_pass_stats(const TileParams& P) {
 
 void QuregImpl::launch_tile() {
     // The tile's high qubits: the pass's pair targets, topped up with the
-    // lowest unused local qubits, so that qubits 5, 6, ... extend the
-    // contiguous 512 B segments into longer runs (fewer, larger bulk copies).
+    // lowest unused local qubits (qubits 5, 6, 7 let a warp's last-phase
+    // segments merge into longer bulk copies, see P.fin_run).
     std::vector<int> high = tile_high;
     for (int q = kLaneQubits; static_cast<int>(high.size()) < kTileHigh && q < local_qubits; ++q)
         if (std::find(high.begin(), high.end(), q) == high.end()) high.push_back(q);
     std::sort(high.begin(), high.end());
-    int seg_run = 0;
-    while (seg_run < kTileHigh && high[seg_run] == kLaneQubits + seg_run) ++seg_run;
     auto tbit = [&](int q) -> int { // tile bit of a local qubit, -1 if outside
         if (q >= 0 && q < kLaneQubits) return q;
         for (int j = 0; j < kTileHigh; ++j)
@@ -422,7 +420,6 @@ void QuregImpl::launch_tile() {
     std::memset(&P, 0, sizeof(P));
     P.num_tiles = uint64_t{1} << (local_qubits - kTileQubits);
     P.num_phases = static_cast<int>(phases.size());
-    P.seg_run = std::min(seg_run, 5); // copies of up to 32 segments (16 KiB)
     for (int j = 0; j < kTileHigh; ++j) P.high_pos[j] = high[j];
     for (int s = 0; s < (1 << kTileHigh); ++s) {
         uint64_t off = 0;

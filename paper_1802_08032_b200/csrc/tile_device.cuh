@@ -4,34 +4,35 @@
 // generated straight-line program for one pass shape).
 //
 // Structure (qgpu_device.h: TileParams / TilePhase / TileOp):
-//  * one persistent CTA per SM walks tiles of 2^12 amplitudes (qubits 0-4 plus
-//    7 higher qubits chosen per pass);
-//  * HBM <-> shared memory through TMA: warp 0 issues cp.async.bulk loads
-//    (completion on an mbarrier) and bulk stores at tile boundaries, three
-//    64 KiB stages deep, so the streaming overlaps the ops and no register
-//    holds data in flight;
+//  * one persistent CTA (16 warps) per SM walks tiles of 2^12 amplitudes
+//    (qubits 0-4 plus 7 higher qubits chosen per pass);
+//  * HBM <-> shared memory through TMA bulk copies, three 64 KiB stages
+//    deep: each warp loads, stores and refills the 8 segments (512 B runs of
+//    qubits 0-4) it owns in the last phase, posting its bytes on the stage's
+//    tx-count mbarrier (16 arrivals per fill) — no end-of-tile block barrier;
 //  * the ops run in phases: every thread holds 8 amplitudes in registers
-//    spanning the phase's 3 register qubits (lanes span qubits 0-4, the 16
-//    warps the remaining 4 tile qubits). Pair ops on register
-//    qubits stay in registers, on lane qubits they use warp shuffles, diagonal
-//    gates and channels are elementwise anywhere; between phases the tile is
-//    re-laid out through shared memory.
+//    spanning the phase's 3 register qubits; lane bits 0-2 span qubits 0-2,
+//    lane bits 3-4 qubits 3-4 or two other tile qubits, the 16 warps the
+//    rest. Pair ops on register qubits stay in registers, on lane qubits
+//    they use warp shuffles, diagonal gates and channels are elementwise
+//    anywhere; between phases the tile is re-laid out through shared memory
+//    behind a barrier over the warps that exchange data (named barriers for
+//    groups, the CTA otherwise).
 //
 // Code-generation notes (each measured with ncu on this kernel):
-//  * the op table is copied to shared memory once per launch — read from the
-//    kernel-parameter bank every op missed the constant cache;
-//  * an op's header and coefficients are loaded one op ahead (OpCtx), so their
-//    latency hides behind the previous op; the op index is warp-uniform, so
-//    the loads address through uniform registers;
-//  * the host resolves each op to one handler code (TileCode), and the build
-//    passes -jump-table-density=1 to NVVM: one brx.idx per op instead of a
-//    binary search tree of compares;
+//  * interpreter: the op table is copied to shared memory once per launch,
+//    an op's header and coefficients are loaded one op ahead (OpCtx), the
+//    host resolves each op to one handler code (TileCode) and the build
+//    passes -jump-table-density=1 to NVVM: one brx.idx per op;
+//  * JIT: the same handlers, called straight-line (step_c<RB, CODE>) with
+//    literal headers and layouts; coefficients as constant-bank operands;
 //  * outer-qubit controls are evaluated once per tile (a ballot per 32 ops),
 //    not per op and phase;
 //  * handlers never branch per element on run-time values (selects only where
 //    lane / register controls need them) — per-element branches made ptxas
 //    copy the whole 64-register tile around them;
-//  * warp-uniform controls (on warp or outer qubits) skip the op outright.
+//  * coefficient signs are applied to register operands (exact), so the
+//    coefficients themselves can stay constant-bank operands.
 #pragma once
 
 #include "pair_math.cuh"
@@ -57,10 +58,6 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
@@ -424,16 +421,6 @@ __device__ __forceinline__ uint64_t tile_gbase_slow(const TileParams& P, uint64_
     return gb;
 }
 
-// All 2^WB warps apply the ops and share the TMA copies at tile boundaries
-// (one bulk copy per thread: a single issuing warp made the others wait at
-// the next phase barrier, 33 % of all stall samples). full[b]: stage b holds
-// a loaded tile (tx-count barrier). After the block barrier that ends tile t,
-// the threads bulk-store stage t % NBUF and refill the stage freed one tile
-// earlier with tile t - 1 + NBUF; each thread waited for its own part of that
-// stage's store to leave shared memory before the barrier, long after it was
-// issued, so the wait never stalls. No separate producer warp: 8 warps (2 per
-// SM sub-partition) may use 255 registers each, where a 9th warp would cap
-// them at 168.
 // The interpreter: the phase body dispatches every op through one jump table
 // (Prog::kInterp); a JIT program replaces it with straight-line code.
 struct Interp {
