@@ -196,6 +196,11 @@ struct TileParams {
     int32_t high_sorted[kTileHigh];        // the same qubits, ascending
     int32_t any_outer;                     // some op has controls outside the tile
     uint64_t seg_off[1 << kTileHigh];      // global offset of tile segment s
+    // the last phase stores straight to HBM: local-index offsets of its
+    // register i, warp w and lane bits 3, 4 (lane bits 0-2: qubits 0-2)
+    uint64_t fin_greg[1 << kPhaseRegBits];
+    uint64_t fin_gwarp[1 << kTileWarpBits];
+    uint64_t fin_glane[2];
     // the 8 segments warp w owns in the last phase (its warp bits fixed)
     uint8_t fin_seg[1 << kTileWarpBits][1 << (kTileHigh - kTileWarpBits)];
     TilePhase phases[kMaxPhases];

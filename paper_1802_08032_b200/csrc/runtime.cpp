@@ -576,6 +576,25 @@ void QuregImpl::launch_tile() {
         }
         for (int j = 0; j < 2; ++j) Q.lane_off[j] = static_cast<uint16_t>(1u << lb[j]);
         if (p + 1 == phases.size()) {
+            // last phase: HBM offsets of its registers, warps and lane bits
+            auto gbit = [&](int t) -> uint64_t {
+                return t < kLaneQubits ? uint64_t{1} << t : uint64_t{1} << high[t - kLaneQubits];
+            };
+            for (int i = 0; i < (1 << kPhaseRegBits); ++i) {
+                uint64_t g = 0;
+                for (int j = 0; j < kPhaseRegBits; ++j)
+                    if ((i >> j) & 1) g |= gbit(rb[j]);
+                P.fin_greg[i] = g;
+            }
+            for (int w = 0; w < (1 << kTileWarpBits); ++w) {
+                uint64_t g = 0;
+                for (int j = 0; j < kTileWarpBits; ++j)
+                    if ((w >> j) & 1) g |= gbit(wb[j]);
+                P.fin_gwarp[w] = g;
+            }
+            for (int j = 0; j < 2; ++j) P.fin_glane[j] = gbit(lb[j]);
+        }
+        if (p + 1 == phases.size()) {
             // last phase: warp w owns the segments whose warp bits are w
             // (tile bits 0-4 are lane or register bits, never warp bits)
             std::vector<int> free_hi;

@@ -474,15 +474,6 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
         if (lane < ncopy) tma_load(buf + my_soff, amps + gb + my_goff, run_bytes, &full[b]);
         if (lane == 0) mbar_expect_tx(&full[b], SEGS * SEG_BYTES);
     };
-    auto store_mine = [&](uint64_t t) {
-        const int b = static_cast<int>(t % NBUF);
-        const uint64_t gb = tile_gbase(blockIdx.x + t * G);
-        double2* buf = smem + (static_cast<size_t>(b) << K);
-        if (lane < ncopy) {
-            tma_store(amps + gb + my_goff, buf + my_soff, run_bytes);
-            tma_commit();
-        }
-    };
     constexpr uint32_t kCopyLanes = SEGS; // one segment (run) per lane (a
     // lane-0 unrolled issue with uniform addresses measured 5 % slower)
     if (threadIdx.x == 0) {
@@ -495,6 +486,9 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
     for (uint64_t t = 0; t < NBUF && t < ntiles; ++t) load_mine(t);
     const int nops = P.phases[nph - 1].op_end;
     const uint32_t sops_addr = smem_u32(sops);
+    // this thread's HBM offset in the last phase (lane bits 0-2: qubits 0-2)
+    const uint64_t fin_thread = P.fin_gwarp[w] + (lane & 7u) + ((lane >> 3) & 1u ? P.fin_glane[0] : 0) +
+                                ((lane >> 4) & 1u ? P.fin_glane[1] : 0);
     {
         const uint64_t* src = reinterpret_cast<const uint64_t*>(P.ops);
         uint64_t* dst = reinterpret_cast<uint64_t*>(sops);
@@ -507,7 +501,8 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
     for (uint64_t t = 0; t < ntiles; ++t) {
         const int b = static_cast<int>(t % NBUF);
         double2* buf = smem + (static_cast<size_t>(b) << K);
-        const uint64_t gbase = tile_gbase(blockIdx.x + t * G) + P.global_offset;
+        const uint64_t gb = tile_gbase(blockIdx.x + t * G);
+        const uint64_t gbase = gb + P.global_offset;
         const uint64_t act = any_outer ? active_ops(sops, nops, gbase, lane) : ~uint64_t{0};
         mbar_wait(&full[b], static_cast<uint32_t>((t / NBUF) & 1));
         bool wrote = false, last_skipped = false; // (uniform per tile)
@@ -567,7 +562,16 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
                     step<RB>(b, a, cb, lane, w, gbase);
                     if (o >= end) break;
                 }
-                if (in_a) {
+                if (ph == nph - 1) { // the last phase stores straight to HBM
+                    double2* out = amps + gb + fin_thread;
+                    if (in_a) {
+#pragma unroll
+                        for (int i = 0; i < R; ++i) __stcs(out + P.fin_greg[i], a[i]);
+                    } else {
+#pragma unroll
+                        for (int i = 0; i < R; ++i) __stcs(out + P.fin_greg[i], b[i]);
+                    }
+                } else if (in_a) {
 #pragma unroll
                     for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = a[i];
                 } else {
@@ -577,22 +581,33 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
             } else {
                 // a generated straight-line program (tile_jit.cpp): the
                 // phase's layout offsets and op sequence are literals
-                Prog::template phase<RB>(ph, m, buf, P, lane, w, gbase, sops_addr);
+                Prog::template phase<RB>(ph, m, buf, amps + gb + fin_thread, P, lane, w, gbase, sops_addr);
             }
         }
-        // the warp's segments hold its own last-phase writes — unless the
-        // last phase was skipped on this tile after an earlier one wrote
-        // (rare: outer controls); then other warps wrote them
-        if (last_skipped && wrote) __syncthreads();
-        fence_proxy_async(); // generic-proxy writes -> visible to the bulk store
-        __syncwarp();
-        store_mine(t);
-        if (t >= 1 && t - 1 + NBUF < ntiles) {
-            if (lane < kCopyLanes) tma_wait_read<1>(); // the store of tile t - 1 left the slot
-            load_mine(t - 1 + NBUF);
+        // The last phase stored its results to HBM. If outer controls skipped
+        // it after an earlier phase wrote (rare), the tile's final values are
+        // in shared memory, written by any warp: sync, then each warp moves
+        // its own last-phase positions. If no phase ran, HBM already holds
+        // the tile.
+        if (last_skipped && wrote) {
+            __syncthreads();
+            const TilePhase& Q = P.phases[nph - 1];
+            const uint32_t wofs = Q.warp_off[w] + (lane & 7u) + ((lane >> 3) & 1u ? Q.lane_off[0] : 0u) +
+                                  ((lane >> 4) & 1u ? Q.lane_off[1] : 0u);
+            double2* out = amps + gb + fin_thread;
+#pragma unroll
+            for (int i = 0; i < R; ++i) __stcs(out + P.fin_greg[i], buf[wofs + Q.reg_off[i]]);
+        }
+        // Every access to this warp's last-phase positions happened before
+        // its last phase (the data-flow barriers order them), and the stores
+        // read registers: the warp refills its slots of this stage with tile
+        // t + NBUF at once.
+        if (t + NBUF < ntiles) {
+            fence_proxy_async(); // its generic reads of the slots before the async refill
+            __syncwarp();
+            load_mine(t + NBUF);
         }
     }
-    if (lane < kCopyLanes) tma_wait_all();
 }
 
 } // namespace
