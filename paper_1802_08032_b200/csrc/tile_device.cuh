@@ -506,6 +506,7 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
         const uint64_t act = any_outer ? active_ops(sops, nops, gbase, lane) : ~uint64_t{0};
         mbar_wait(&full[b], static_cast<uint32_t>((t / NBUF) & 1));
         bool wrote = false, last_skipped = false; // (uniform per tile)
+        if constexpr (Prog::kInterp) {
         int prev_ph = -1;                         // the last phase executed
         for (int ph = 0; ph < nph; ++ph) {
             const TilePhase& Q = P.phases[ph];
@@ -578,11 +579,13 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
 #pragma unroll
                     for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = b[i];
                 }
-            } else {
-                // a generated straight-line program (tile_jit.cpp): the
-                // phase's layout offsets and op sequence are literals
-                Prog::template phase<RB>(ph, m, buf, amps + gb + fin_thread, P, lane, w, gbase, sops_addr);
             }
+        }
+        } else {
+            // a generated program (tile_jit.cpp): the whole phase sequence
+            // straight-line, with literal op masks, layouts, barriers and ops
+            Prog::template tile<RB, WB>(act, buf, amps + gb + fin_thread, P, lane, w, gbase, sops_addr, wrote,
+                                        last_skipped);
         }
         // The last phase stored its results to HBM. If outer controls skipped
         // it after an earlier phase wrote (rare), the tile's final values are
