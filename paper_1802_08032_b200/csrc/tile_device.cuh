@@ -96,6 +96,24 @@ __device__ __forceinline__ void tma_wait_read() {
 
 __device__ __forceinline__ void tma_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
+// 16-byte shared-memory accesses as single v2.f64 instructions: left to
+// itself ptxas split some into two 8-byte accesses when the two doubles sat
+// in non-adjacent registers, which made 2-way bank conflicts (ncu: 26 %
+// excess wavefronts in JIT kernels)
+#ifdef QGPU_PLAIN_SMEM
+__device__ __forceinline__ double2 lds16(const double2* p) { return *p; }
+__device__ __forceinline__ void sts16(double2* p, double2 v) { *p = v; }
+#else
+__device__ __forceinline__ double2 lds16(const double2* p) {
+    double2 v;
+    asm volatile("ld.shared.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "r"(smem_u32(p)));
+    return v;
+}
+__device__ __forceinline__ void sts16(double2* p, double2 v) {
+    asm volatile("st.shared.v2.f64 [%0], {%1, %2};" ::"r"(smem_u32(p)), "d"(v.x), "d"(v.y) : "memory");
+}
+#endif
+
 __device__ __forceinline__ void fence_proxy_async() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
 }
@@ -538,7 +556,7 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
                                       ((lane >> 4) & 1u ? Q.lane_off[1] : 0u);
                 double2 a[R], b[R];
 #pragma unroll
-                for (int i = 0; i < R; ++i) a[i] = buf[wofs + Q.reg_off[i]];
+                for (int i = 0; i < R; ++i) a[i] = lds16(buf + wofs + Q.reg_off[i]);
                 bool in_a = true; // the phase's result is in a (else b)
                 // ops alternate a -> b, b -> a; the contexts alternate too,
                 // each loaded one op ahead. `runm` has a bit per op that runs
@@ -574,10 +592,10 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
                     }
                 } else if (in_a) {
 #pragma unroll
-                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = a[i];
+                    for (int i = 0; i < R; ++i) sts16(buf + wofs + Q.reg_off[i], a[i]);
                 } else {
 #pragma unroll
-                    for (int i = 0; i < R; ++i) buf[wofs + Q.reg_off[i]] = b[i];
+                    for (int i = 0; i < R; ++i) sts16(buf + wofs + Q.reg_off[i], b[i]);
                 }
             }
         }
