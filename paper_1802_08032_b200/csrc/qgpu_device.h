@@ -143,6 +143,7 @@ enum TileCode : uint8_t {
     TC_DIAG_UNIFORM_SEL = 48,
     TC_DEPHASE = 49,
     TC_COLLAPSE = 50,
+    TC_DEPOL = 51, // + register-bit pair (0,1) (0,2) (0,3) (1,2) (1,3) (2,3): 51..56
 };
 
 // Op header packed in one 64-bit word (one constant-bank load per op):
@@ -184,7 +185,9 @@ struct TilePhase {
     uint16_t op_begin, op_end;
     // warp bits shared with the previous phase at the same (top) positions:
     // the transition into this phase syncs groups of 2^(WB - sync_bits) warps
+    // on named barriers bar_base + group (each transition its own IDs)
     uint16_t sync_bits;
+    uint16_t bar_base;
 };
 
 struct TileParams {

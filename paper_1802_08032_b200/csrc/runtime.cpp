@@ -267,6 +267,34 @@ bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
     return true;
 }
 
+// A depolarising channel needs both its qubits as register qubits of one
+// phase (its 4-groups span both bits).
+bool QuregImpl::place_tile_depol(const FlatOp& op) {
+    if (phases.empty()) phases.push_back(PhaseState{});
+    auto has = [](const std::vector<int>& v, int x) { return std::find(v.begin(), v.end(), x) != v.end(); };
+    int new_high = 0;
+    for (int q : {op.q0, op.q1})
+        if (q >= kLaneQubits && !has(tile_high, q)) ++new_high;
+    if (static_cast<int>(tile_high.size()) + new_high > env->tile_targets) return false;
+    PhaseState* ph = &phases.back();
+    int need = 0;
+    for (int q : {op.q0, op.q1})
+        if (!has(ph->regs, q)) ++need;
+    if (static_cast<int>(ph->regs.size()) + need > kPhaseRegBits) {
+        if (static_cast<int>(phases.size()) >= max_phases()) return false;
+        PhaseState next;
+        next.op_begin = static_cast<int>(pending.size());
+        phases.push_back(next);
+        ph = &phases.back();
+    }
+    for (int q : {op.q0, op.q1}) {
+        if (!has(ph->regs, q)) ph->regs.push_back(q);
+        if (q >= kLaneQubits && !has(tile_high, q)) tile_high.push_back(q);
+    }
+    pending.push_back(op);
+    return true;
+}
+
 void QuregImpl::enqueue(const FlatOp& lop) {
     if (!swaps_on()) {
         enqueue_phys(lop);
@@ -317,8 +345,20 @@ void QuregImpl::drain(size_t count) {
 void QuregImpl::enqueue_phys(const FlatOp& op) {
     const bool pair = op.kind == FK_GATE && op.cls != CLS_DIAG;
     if (op.kind == FK_DEPOL) {
-        flush_pass();
-        run_depol(op);
+        // fused into the tile pass when both qubits can be register qubits
+        // of a phase (not lane-only qubits 0-2); else its own pass
+        const bool fusable = use_tile() && env->fusion_mode == 0 && op.q0 >= kFixedLaneBits &&
+                             op.q1 >= kFixedLaneBits && op.q0 < local_qubits && op.q1 < local_qubits;
+        if (!fusable) {
+            flush_pass();
+            run_depol(op);
+            return;
+        }
+        if (!place_tile_depol(op)) {
+            flush_pass();
+            place_tile_depol(op);
+        }
+        if (static_cast<int>(pending.size()) >= std::min(env->max_ops, kMaxTileOps)) flush_pass();
         return;
     }
     if (pair && op.q0 >= local_qubits) {
@@ -516,6 +556,24 @@ void QuregImpl::launch_tile() {
             ++c;
         sync_bits[p] = c;
     }
+    // named barrier IDs 1..15: each transition its own range of 2^c IDs (a
+    // shared ID let a lagging warp of one transition complete another's
+    // barrier, and mixed thread counts trap); transitions that do not fit
+    // sync the whole CTA
+    std::vector<int> bar_base(nph, 0);
+    {
+        int next_id = 1;
+        for (size_t p = 1; p < nph; ++p) {
+            const int c = sync_bits[p];
+            if (c == 0 || c >= kTileWarpBits) continue; // CTA barrier / warp sync
+            if (next_id + (1 << c) > 16) {
+                sync_bits[p] = 0;
+                continue;
+            }
+            bar_base[p] = next_id;
+            next_id += 1 << c;
+        }
+    }
     // Renumber the high tile bits so the last phase's non-warp high bits sit
     // at tile bits 5..7 in ascending qubit order: each warp's 8 last-phase
     // segments are then contiguous in shared memory, and whenever those
@@ -562,6 +620,7 @@ void QuregImpl::launch_tile() {
         const std::vector<int>& lb = LB[p];
         const std::vector<int>& wb = WBv[p];
         Q.sync_bits = static_cast<uint16_t>(sync_bits[p]);
+        Q.bar_base = static_cast<uint16_t>(bar_base[p]);
         for (int i = 0; i < (1 << kPhaseRegBits); ++i) {
             uint32_t off = 0;
             for (int j = 0; j < kPhaseRegBits; ++j)
@@ -672,7 +731,13 @@ void QuregImpl::launch_tile() {
             // codes), outer controls skip the op per tile
             const bool ctrl = lane_cm != 0 || reg_cm != 0 || warp_cm != 0;
             uint32_t code;
-            if (op.kind == FK_DEPHASE) {
+            if (op.kind == FK_DEPOL) {
+                if (q0k != TL_REG || q1k != TL_REG)
+                    throw DeviceError("internal: a fused depolarising channel needs register qubits");
+                const int j0 = std::min(q0p, q1p), j1 = std::max(q0p, q1p);
+                static const int pair_index[4][4] = {{-1, 0, 1, 2}, {-1, -1, 3, 4}, {-1, -1, -1, 5}, {-1, -1, -1, -1}};
+                code = TC_DEPOL + pair_index[j0][j1];
+            } else if (op.kind == FK_DEPHASE) {
                 code = TC_DEPHASE;
             } else if (op.kind == FK_COLLAPSE) {
                 code = TC_COLLAPSE;

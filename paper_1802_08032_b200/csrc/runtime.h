@@ -179,6 +179,7 @@ struct QuregImpl {
     int pass_H() const;
     bool use_tile() const;
     bool place_tile(const FlatOp& op, bool pair);
+    bool place_tile_depol(const FlatOp& op);
     int max_phases() const;
     void launch_tile();
     void run_simple(const FlatOp& op);

@@ -390,6 +390,26 @@ __device__ __forceinline__ void step_c(const Regs<RB>& s, Regs<RB>& d, const OpC
             const double k = on ? sc : 1.0; // x * 1.0 is exact
             d[i] = make_double2(s[i].x * k, s[i].y * k);
         }
+    } else if constexpr (CODE >= TC_DEPOL && CODE < TC_DEPOL + 6) {
+        // depolarising on register bits J0 < J1 (t and t+N of a density
+        // matrix), the arithmetic of k_depolarise (density.cpp:62-81): the
+        // 00 / 11 corners mix, the off-diagonal corners scale
+        constexpr int pi = CODE - TC_DEPOL;
+        constexpr int J0 = pi < 3 ? 0 : pi < 5 ? 1 : 2;
+        constexpr int J1 = pi == 0 ? 1 : pi == 1 ? 2 : pi == 2 ? 3 : pi == 3 ? 2 : 3;
+        if constexpr (J1 < RB) {
+            const double keep = c[0], swap = c[1], off = c[2];
+#pragma unroll
+            for (int i = 0; i < (1 << RB); ++i) {
+                if (i & ((1 << J0) | (1 << J1))) continue;
+                const int i01 = i | (1 << J0), i10 = i | (1 << J1), i11 = i01 | i10;
+                const double2 d0 = s[i], d1 = s[i11];
+                d[i] = make_double2(fma(swap, d1.x, keep * d0.x), fma(swap, d1.y, keep * d0.y));
+                d[i11] = make_double2(fma(swap, d0.x, keep * d1.x), fma(swap, d0.y, keep * d1.y));
+                d[i01] = make_double2(s[i01].x * off, s[i01].y * off);
+                d[i10] = make_double2(s[i10].x * off, s[i10].y * off);
+            }
+        }
     } else if constexpr (CODE == TC_COLLAPSE) { // keep bit(q0) (and bit(q1)) == outcome, scaled
         const uint32_t flags = (h >> 6) & 15u;
         const uint32_t q0k = (h >> 11) & 3u, q1k = (h >> 19) & 3u, q1p = (h >> 21) & 63u;
@@ -421,7 +441,8 @@ __device__ __forceinline__ void step(const Regs<RB>& s, Regs<RB>& d, const OpCtx
 #define QGPU_CASE8(K) QGPU_CASE(K) QGPU_CASE(K + 1) QGPU_CASE(K + 2) QGPU_CASE(K + 3) \
     QGPU_CASE(K + 4) QGPU_CASE(K + 5) QGPU_CASE(K + 6) QGPU_CASE(K + 7)
         QGPU_CASE8(0) QGPU_CASE8(8) QGPU_CASE8(16) QGPU_CASE8(24) QGPU_CASE8(32) QGPU_CASE8(40)
-        QGPU_CASE(48) QGPU_CASE(49) QGPU_CASE(50)
+        QGPU_CASE(48) QGPU_CASE(49) QGPU_CASE(50) QGPU_CASE(51) QGPU_CASE(52) QGPU_CASE(53)
+        QGPU_CASE(54) QGPU_CASE(55) QGPU_CASE(56)
 #undef QGPU_CASE8
 #undef QGPU_CASE
     default: __builtin_unreachable(); // the host emits TileCode values only
@@ -546,7 +567,7 @@ __device__ __forceinline__ void tile_pass_body(double2* __restrict__ amps, const
                 else if (c >= WB)
                     __syncwarp();
                 else
-                    asm volatile("bar.sync %0, %1;" ::"r"(1 + (w >> (WB - c))), "r"(32 << (WB - c))
+                    asm volatile("bar.sync %0, %1;" ::"r"(Q.bar_base + (w >> (WB - c))), "r"(32 << (WB - c))
                                  : "memory");
             }
             wrote = true;
