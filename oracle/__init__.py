@@ -83,6 +83,7 @@ def ref():
         L.ref_last_error.argtypes = [ctypes.c_char_p, ctypes.c_int]
         L.ref_kernel_invocations.restype = ctypes.c_ulonglong
         L.ref_run_ops.argtypes = [ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp, ctypes.c_int, _vp]
+        L.ref_run_ops_single.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, _vp]
         L.ref_count_kernel_calls.argtypes = [ctypes.c_int, ctypes.c_int, _vp, ctypes.POINTER(ctypes.c_ulonglong)]
         L.ref_set_get.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong, ctypes.c_double, ctypes.c_double, _dp, _dp]
         L.ref_reductions.argtypes = [ctypes.c_int, ctypes.c_int, _vp, _dp, _dp, _dp, _dp]
@@ -113,6 +114,8 @@ def restated():
         L.orc_pair_base_index.restype = _u64
         L.orc_pair_base_index.argtypes = [_u64, ctypes.c_int]
         L.orc_apply_gate.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _u64, _vp]
+        L.orc_run_ops_f.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, _vp]
+        L.orc_run_ops_f.restype = ctypes.c_int
         L.orc_apply_dm_gate.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _u64, _vp]
         L.orc_dephase.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double]
         L.orc_depolarise.argtypes = [_vp, ctypes.c_int, ctypes.c_int, ctypes.c_double]
@@ -283,4 +286,28 @@ def orc_combine(mine: np.ndarray, theirs: np.ndarray, low_mask: int, own_lo: boo
     theirs = np.ascontiguousarray(theirs, dtype=np.complex128)
     m = np.ascontiguousarray(m, dtype=np.float64)
     restated().orc_combine(_ptr(out), _ptr(theirs), out.size, low_mask, int(own_lo), _ptr(m))
+    return out
+
+
+def zero_state_f(nq: int, density: bool = False) -> np.ndarray:
+    """Single-precision zero state (complex64)."""
+    n = 1 << (2 * nq if density else nq)
+    a = np.zeros(n, dtype=np.complex64)
+    a[0] = 1.0
+    return a
+
+
+def orc_run_f(nq: int, ops, density: bool = False) -> np.ndarray:
+    """The single-precision restatement (complex64 result)."""
+    ops = as_ops(ops)
+    amps = zero_state_f(nq, density)
+    _check(restated().orc_run_ops_f(nq, int(density), len(ops), _ptr(ops), _ptr(amps)))
+    return amps
+
+
+def ref_run_single(nq: int, ops, density: bool = False, workers: int = 1) -> np.ndarray:
+    """The compiled reference in Precision::Single (complex64 result)."""
+    ops = as_ops(ops)
+    out = np.zeros(1 << (2 * nq if density else nq), dtype=np.complex64)
+    _check(ref().ref_run_ops_single(nq, int(density), len(ops), _ptr(ops), workers, _ptr(out)))
     return out

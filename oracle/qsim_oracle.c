@@ -337,3 +337,99 @@ void orc_combine(double* mine, const double* theirs, uint64_t len,
         mine[2 * i + 1] = out[1];
     }
 }
+
+/* ------------------------------------------------------ single precision
+ *
+ * The reference's float instantiation (kernels.cpp:61-62, density.cpp:105-
+ * 140): Mat2<float> narrows the gate matrix (pair_math.hpp:14-24), the same
+ * pair expressions evaluate in float, the channel factors are narrowed once
+ * (static_cast<T>(1 - 2p) etc.). Restated with the float form of the
+ * double path's fma chain; pinned against the compiled reference's
+ * Precision::Single run (tests/test_oracle.py). */
+
+static inline void pair_out_f(const float* lo, const float* hi, const float* m, float* out) {
+    const float lr = lo[0], li = lo[1], hr = hi[0], hi_ = hi[1];
+    out[0] = fmaf(-m[3], hi_, fmaf(m[2], hr, fmaf(m[0], lr, -(m[1] * li))));
+    out[1] = fmaf(m[3], hr, fmaf(m[2], hi_, fmaf(m[0], li, m[1] * lr)));
+}
+
+void orc_apply_gate_f(float* amps, int nq, int target, uint64_t ctrl_mask, const double* md) {
+    float m[8];
+    for (int k = 0; k < 8; ++k) m[k] = (float)md[k];
+    const uint64_t num_pairs = UINT64_C(1) << (nq - 1);
+    const uint64_t off = UINT64_C(1) << target;
+    for (uint64_t i = 0; i < num_pairs; ++i) {
+        const uint64_t base = orc_pair_base_index(i, target);
+        if ((base & ctrl_mask) != ctrl_mask)
+            continue;
+        float* lo = amps + 2 * base;
+        float* hi = amps + 2 * (base + off);
+        float nl[2], nh[2];
+        pair_out_f(lo, hi, m, nl);
+        pair_out_f(lo, hi, m + 4, nh);
+        lo[0] = nl[0]; lo[1] = nl[1];
+        hi[0] = nh[0]; hi[1] = nh[1];
+    }
+}
+
+static void orc_channel_f(float* amps, int n, int target, double prob, int depol) {
+    const int flat = 2 * n;
+    const uint64_t row = UINT64_C(1) << target;
+    const uint64_t col = UINT64_C(1) << (target + n);
+    const float scale = (float)(1.0 - 2.0 * prob);
+    const float keep = (float)(1.0 - 2.0 * prob / 3.0);
+    const float swap = (float)(2.0 * prob / 3.0);
+    const float offs = (float)(1.0 - 4.0 * prob / 3.0);
+    const uint64_t count = UINT64_C(1) << (flat - 2);
+    for (uint64_t u = 0; u < count; ++u) {
+        const uint64_t n00 = insert_zero_bit(insert_zero_bit(u, target), target + n);
+        float* a = amps + 2 * (n00 | row);
+        float* b = amps + 2 * (n00 | col);
+        if (depol) {
+            float* p0 = amps + 2 * n00;
+            float* p1 = amps + 2 * (n00 | row | col);
+            const float d0r = p0[0], d0i = p0[1], d1r = p1[0], d1i = p1[1];
+            p0[0] = fmaf(swap, d1r, keep * d0r);
+            p0[1] = fmaf(swap, d1i, keep * d0i);
+            p1[0] = fmaf(swap, d0r, keep * d1r);
+            p1[1] = fmaf(swap, d0i, keep * d1i);
+            a[0] *= offs; a[1] *= offs;
+            b[0] *= offs; b[1] *= offs;
+        } else {
+            a[0] *= scale; a[1] *= scale;
+            b[0] *= scale; b[1] *= scale;
+        }
+    }
+}
+
+int orc_run_ops_f(int nq, int density, int nops, const orc_op* ops, float* amps) {
+    for (int i = 0; i < nops; ++i) {
+        const orc_op* op = ops + i;
+        switch (op->kind) {
+        case ORC_GATE:
+            if (density) {
+                double conj[8];
+                for (int j = 0; j < 4; ++j) {
+                    conj[2 * j] = op->m[2 * j];
+                    conj[2 * j + 1] = -op->m[2 * j + 1];
+                }
+                orc_apply_gate_f(amps, 2 * nq, op->target, op->ctrl_mask, op->m);
+                orc_apply_gate_f(amps, 2 * nq, op->target + nq, op->ctrl_mask << nq, conj);
+            } else {
+                orc_apply_gate_f(amps, nq, op->target, op->ctrl_mask, op->m);
+            }
+            break;
+        case ORC_DEPHASE:
+            if (!density) return 1;
+            orc_channel_f(amps, nq, op->target, op->param, 0);
+            break;
+        case ORC_DEPOLARISE:
+            if (!density) return 1;
+            orc_channel_f(amps, nq, op->target, op->param, 1);
+            break;
+        default:
+            return 1;
+        }
+    }
+    return 0;
+}

@@ -137,6 +137,19 @@ int ref_run_ops(int num_qubits, int density, const double* init, int nops,
     });
 }
 
+// The same in the reference's single precision (Precision::Single: complex
+// float amplitudes, Mat2<float>); `out` receives interleaved floats.
+int ref_run_ops_single(int num_qubits, int density, int nops, const orc_op* ops, int workers,
+                       float* out) {
+    return guarded([&] {
+        qsim::Register reg(num_qubits, kind_of(density), qsim::Precision::Single);
+        for (int i = 0; i < nops; ++i)
+            apply_one(reg, ops[i], workers);
+        if (out)
+            std::memcpy(out, reg.amps().data32(), reg.amps().byte_size());
+    });
+}
+
 // Per-op counter of core-kernel entries (kernels.cpp:15-20, 47).
 int ref_count_kernel_calls(int num_qubits, int density, const orc_op* op,
                            unsigned long long* calls) {

@@ -121,3 +121,18 @@ def test_combine_restatement_matches_reference_distributed(strategy):
                 new.append(oracle.orc_combine(chunks[r], chunks[peer], low, own_lo, op["m"]))
         chunks = new
     assert bits_equal(np.concatenate(chunks), ref_out)
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="reference not built here")
+@pytest.mark.parametrize("n,density,seed", [(8, False, 1), (11, False, 2), (5, True, 3), (13, False, 4)])
+def test_single_precision_restatement_matches_reference(n, density, seed):
+    """The float restatement (Mat2<float>, float fma chain, narrowed channel
+    factors) equals the reference's Precision::Single run bit for bit."""
+    import numpy as np
+
+    from tests.harness import random_gate_circuit, to_oracle_ops
+
+    ops = to_oracle_ops(random_gate_circuit(n, 200, seed, max_controls=2, channels=density))
+    got = oracle.orc_run_f(n, ops, density)
+    want = oracle.ref_run_single(n, ops, density)
+    assert got.dtype == np.complex64 and np.array_equal(got, want)
