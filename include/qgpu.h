@@ -56,6 +56,17 @@ int qgpuGetDevice(QuESTEnv env);
 void qgpuProfileStart(QuESTEnv env);
 int qgpuProfileStop(QuESTEnv env, double* ms, int* kinds, int maxRecords);
 
+/* ------------------------------------------------------------- precision */
+/* Register(num_qubits, kind, precision) (register.hpp:53-54): precision 1 =
+ * Precision::Single (float2 amplitudes, float arithmetic: Mat2<float> and
+ * channel factors narrowed once, kernels.cpp:61-62, density.cpp:105-140),
+ * 2 = Precision::Double (what createQureg / createDensityQureg make). The
+ * host boundary stays double: reads widen, writes narrow (register.cpp:
+ * 30-51); reductions accumulate in double. Single-precision registers of
+ * fewer than 12 local qubits run one kernel per op. */
+Qureg qgpuCreateQuregPrecision(int numQubits, QuESTEnv env, int density, int precision);
+int qgpuGetPrecision(Qureg qureg); /* 1 or 2; -1 on error */
+
 /* --------------------------------------------------------- bulk state I/O */
 /* Interleaved (re, im) doubles of flat amplitudes [start, start + num). */
 void qgpuCopyStateToHost(Qureg qureg, long long int start, long long int num, double* out);
@@ -146,14 +157,15 @@ int qgpuModeledBytesPerRank(int numQubits, int rankLog2, int strategy, int singl
                             unsigned long long blockAmps, unsigned long long* bytes);
 int qgpuMaxQubits(unsigned long long nodeBytes, unsigned long long overheadBytes, int strategy,
                   int singlePrecision, int rankLog2);
-/* This runtime's device footprint per rank: the partition (16 B x
+/* This runtime's device footprint per rank: the partition (16 B, or 8 B single, x
  * 2^(flat - k)), two exchange sub-chunk buffers of chunkAmps amplitudes once
  * k > 0, and the reduction scratch; and the largest register (qubits, or N
  * of an N-qubit density matrix) whose footprint fits deviceBytes.
  * createQureg preflights against free HBM with the same numbers. */
-unsigned long long qgpuDeviceBytesPerRank(int flatQubits, int rankLog2, unsigned long long chunkAmps);
+unsigned long long qgpuDeviceBytesPerRank(int flatQubits, int rankLog2, unsigned long long chunkAmps,
+                                          int singlePrecision);
 int qgpuDeviceMaxQubits(unsigned long long deviceBytes, int rankLog2, unsigned long long chunkAmps,
-                        int density);
+                        int density, int singlePrecision);
 
 #ifdef __cplusplus
 }

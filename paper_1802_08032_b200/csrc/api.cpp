@@ -516,15 +516,28 @@ Qureg createDensityQureg(int numQubits, QuESTEnv env) {
                    [&] { return make_handle(create_register(env_of(env), numQubits, true)); });
 }
 
+Qureg qgpuCreateQuregPrecision(int numQubits, QuESTEnv env, int density, int precision) {
+    return guarded("qgpuCreateQuregPrecision", null_qureg(), [&] {
+        if (precision != 1 && precision != 2)
+            throw qgpu::DomainError("precision must be 1 (single) or 2 (double), got " +
+                                    std::to_string(precision));
+        return make_handle(create_register(env_of(env), numQubits, density != 0, precision == 1));
+    });
+}
+
+int qgpuGetPrecision(Qureg qureg) {
+    return guarded("qgpuGetPrecision", -1, [&] { return reg_of(qureg)->single ? 1 : 2; });
+}
+
 Qureg createCloneQureg(Qureg qureg, QuESTEnv env) {
     return guarded("createCloneQureg", null_qureg(), [&] {
         QuregImpl* src = reg_of(qureg);
-        QuregImpl* r = create_register(env_of(env), src->N, src->density);
+        QuregImpl* r = create_register(env_of(env), src->N, src->density, src->single);
         src->flush();
         r->sp = src->sp; // same logical -> physical qubit map
         for (size_t k = 0; k < r->shards.size(); ++k)
             cuda_check(cudaMemcpyAsync(r->shards[k].amps, src->shards[k].amps,
-                                       r->local_len * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                       r->local_len * r->amp_bytes(), cudaMemcpyDeviceToDevice,
                                        src->env->stream),
                        "clone");
         cuda_check(cudaStreamSynchronize(src->env->stream), "clone");
@@ -591,7 +604,7 @@ void initPlusState(Qureg qureg) {
         r->discard();
         const double v = r->density ? 1.0 / static_cast<double>(uint64_t{1} << r->N)
                                     : 1.0 / std::sqrt(static_cast<double>(uint64_t{1} << r->N));
-        for (auto& s : r->shards) launch_fill(s.amps, r->local_len, make_double2(v, 0.0), r->env->stream);
+        for (auto& s : r->shards) launch_fill(s.amps, r->single, r->local_len, v, 0.0, r->env->stream);
         cuda_check(cudaGetLastError(), "initPlusState");
     });
 }
@@ -674,14 +687,14 @@ void cloneQureg(Qureg targetQureg, Qureg copyQureg) {
     guarded_void("cloneQureg", [&] {
         QuregImpl* t = reg_of(targetQureg);
         QuregImpl* c = reg_of(copyQureg);
-        if (t->density != c->density || t->N != c->N || t->env != c->env)
-            throw qgpu::DomainError("cloneQureg needs registers of the same kind and size");
+        if (t->density != c->density || t->N != c->N || t->env != c->env || t->single != c->single)
+            throw qgpu::DomainError("cloneQureg needs registers of the same kind, size and precision");
         c->flush();
         t->discard_all();
         t->sp = c->sp;
         for (size_t k = 0; k < t->shards.size(); ++k)
             cuda_check(cudaMemcpyAsync(t->shards[k].amps, c->shards[k].amps,
-                                       t->local_len * sizeof(double2), cudaMemcpyDeviceToDevice,
+                                       t->local_len * t->amp_bytes(), cudaMemcpyDeviceToDevice,
                                        t->env->stream),
                        "cloneQureg");
     });
@@ -1034,16 +1047,18 @@ int qgpuMaxQubits(unsigned long long nodeBytes, unsigned long long overheadBytes
     });
 }
 
-unsigned long long qgpuDeviceBytesPerRank(int flatQubits, int rankLog2, unsigned long long chunkAmps) {
+unsigned long long qgpuDeviceBytesPerRank(int flatQubits, int rankLog2, unsigned long long chunkAmps,
+                                          int singlePrecision) {
     return guarded("qgpuDeviceBytesPerRank", 0ull, [&] {
-        return static_cast<unsigned long long>(qgpu::device_bytes_per_rank(flatQubits, rankLog2, chunkAmps));
+        return static_cast<unsigned long long>(
+            qgpu::device_bytes_per_rank(flatQubits, rankLog2, chunkAmps, singlePrecision != 0));
     });
 }
 
 int qgpuDeviceMaxQubits(unsigned long long deviceBytes, int rankLog2, unsigned long long chunkAmps,
-                        int density) {
+                        int density, int singlePrecision) {
     return guarded("qgpuDeviceMaxQubits", -1, [&] {
-        return qgpu::device_max_qubits(deviceBytes, rankLog2, chunkAmps, density != 0);
+        return qgpu::device_max_qubits(deviceBytes, rankLog2, chunkAmps, density != 0, singlePrecision != 0);
     });
 }
 

@@ -164,23 +164,40 @@ inline unsigned grid_for(uint64_t work, int threads, unsigned cap = 148u * 16u) 
     return static_cast<unsigned>(blocks);
 }
 
-template <int CLS>
-__global__ void k_gate_simple(double2* __restrict__ amps, uint64_t num_pairs, int t,
-                              uint64_t cmask, Mat2 m) {
+// The simple kernels are instantiated for both precisions: V = double2 / R =
+// double, or V = float2 / R = float (the reference's Precision::Single:
+// Mat2<float> narrows the gate matrix, channel factors are narrowed once,
+// kernels.cpp:61-62, density.cpp:105-140).
+template <class R> struct MatT { R m[8]; };
+
+template <class R> MatT<R> narrow(const Mat2& m) {
+    MatT<R> r;
+    for (int k = 0; k < 8; ++k) r.m[k] = static_cast<R>(m.m[k]);
+    return r;
+}
+
+template <class V> struct RealOf;
+template <> struct RealOf<double2> { using type = double; };
+template <> struct RealOf<float2> { using type = float; };
+
+template <int CLS, class V, class R>
+__global__ void k_gate_simple(V* __restrict__ amps, uint64_t num_pairs, int t, uint64_t cmask,
+                              MatT<R> m) {
     const uint64_t off = uint64_t{1} << t;
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x;
          i < num_pairs; i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t base = pair_base_index(i, t);
         if ((base & cmask) != cmask) continue;
-        double2 lo = amps[base], hi = amps[base + off];
+        V lo = amps[base], hi = amps[base + off];
         pair_update<CLS>(lo, hi, m.m);
         amps[base] = lo;
         amps[base + off] = hi;
     }
 }
 
-__global__ void k_diag_simple(double2* __restrict__ amps, uint64_t len, uint64_t goff,
-                              int t, uint64_t cmask, Mat2 m, uint8_t flags) {
+template <class V, class R>
+__global__ void k_diag_simple(V* __restrict__ amps, uint64_t len, uint64_t goff, int t,
+                              uint64_t cmask, MatT<R> m, uint8_t flags) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t g = goff + i;
@@ -191,13 +208,14 @@ __global__ void k_diag_simple(double2* __restrict__ amps, uint64_t len, uint64_t
     }
 }
 
-__global__ void k_dephase(double2* __restrict__ amps, uint64_t len, uint64_t goff, int q0,
-                          int q1, double scale) {
+template <class V, class R>
+__global__ void k_dephase(V* __restrict__ amps, uint64_t len, uint64_t goff, int q0, int q1,
+                          R scale) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t g = goff + i;
         if (((g >> q0) & 1u) != ((g >> q1) & 1u)) {
-            double2 a = amps[i];
+            V a = amps[i];
             a.x *= scale;
             a.y *= scale;
             amps[i] = a;
@@ -205,38 +223,41 @@ __global__ void k_dephase(double2* __restrict__ amps, uint64_t len, uint64_t gof
     }
 }
 
-__global__ void k_collapse(double2* __restrict__ amps, uint64_t len, uint64_t goff, int q0,
-                           int q1, int outcome, double scale) {
+template <class V, class R>
+__global__ void k_collapse(V* __restrict__ amps, uint64_t len, uint64_t goff, int q0, int q1,
+                           int outcome, R scale) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const uint64_t g = goff + i;
         const bool keep = static_cast<int>((g >> q0) & 1u) == outcome &&
                           (q1 < 0 || static_cast<int>((g >> q1) & 1u) == outcome);
+        V a = amps[i];
         if (keep) {
-            double2 a = amps[i];
             a.x *= scale;
             a.y *= scale;
-            amps[i] = a;
         } else {
-            amps[i] = make_double2(0.0, 0.0);
+            a.x = R(0);
+            a.y = R(0);
         }
+        amps[i] = a;
     }
 }
 
 // density.cpp:62-81 (keep/swap diagonal mix uses the reference's contraction:
 // fma(swap, other, keep * own)).
-__global__ void k_depolarise(double2* __restrict__ amps, uint64_t count, int t, int tN,
-                             double keep, double swap, double off) {
+template <class V, class R>
+__global__ void k_depolarise(V* __restrict__ amps, uint64_t count, int t, int tN, R keep,
+                             R swap, R off) {
     const uint64_t row = uint64_t{1} << t, col = uint64_t{1} << tN;
     for (uint64_t u = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; u < count;
          u += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         // the two bits in either order (the swap layer may permute them)
         const uint64_t n00 = insert_zero_bit(insert_zero_bit(u, t < tN ? t : tN), t < tN ? tN : t);
         const uint64_t n11 = n00 | row | col;
-        const double2 d0 = amps[n00], d1 = amps[n11];
-        amps[n00] = make_double2(fma(swap, d1.x, keep * d0.x), fma(swap, d1.y, keep * d0.y));
-        amps[n11] = make_double2(fma(swap, d0.x, keep * d1.x), fma(swap, d0.y, keep * d1.y));
-        double2 a = amps[n00 | row], c = amps[n00 | col];
+        const V d0 = amps[n00], d1 = amps[n11];
+        amps[n00] = V{fma(swap, d1.x, keep * d0.x), fma(swap, d1.y, keep * d0.y)};
+        amps[n11] = V{fma(swap, d0.x, keep * d1.x), fma(swap, d0.y, keep * d1.y)};
+        V a = amps[n00 | row], c = amps[n00 | col];
         a.x *= off; a.y *= off;
         c.x *= off; c.y *= off;
         amps[n00 | row] = a;
@@ -244,13 +265,13 @@ __global__ void k_depolarise(double2* __restrict__ amps, uint64_t count, int t, 
     }
 }
 
-template <int CLS>
-__global__ void k_combine(double2* __restrict__ mine, const double2* __restrict__ theirs,
-                          uint64_t len, uint64_t idx0, uint64_t low_mask, int own_lo, Mat2 m) {
+template <int CLS, class V, class R>
+__global__ void k_combine(V* __restrict__ mine, const V* __restrict__ theirs, uint64_t len,
+                          uint64_t idx0, uint64_t low_mask, int own_lo, MatT<R> m) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         if (((idx0 + i) & low_mask) != low_mask) continue;
-        double2 lo, hi;
+        V lo, hi;
         if (own_lo) {
             lo = mine[i];
             hi = theirs[i];
@@ -263,19 +284,19 @@ __global__ void k_combine(double2* __restrict__ mine, const double2* __restrict_
     }
 }
 
-__global__ void k_combine_depol(double2* __restrict__ mine, const double2* __restrict__ theirs,
-                                uint64_t len, uint64_t idx0, int t, int own_col, double keep,
-                                double swap, double off) {
+template <class V, class R>
+__global__ void k_combine_depol(V* __restrict__ mine, const V* __restrict__ theirs, uint64_t len,
+                                uint64_t idx0, int t, int own_col, R keep, R swap, R off) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
         const int r = static_cast<int>(((idx0 + i) >> t) & 1u);
-        double2 a = mine[i];
+        V a = mine[i];
         if (r != own_col) {
             a.x *= off;
             a.y *= off;
         } else {
-            const double2 o = theirs[i ^ (uint64_t{1} << t)];
-            a = make_double2(fma(swap, o.x, keep * a.x), fma(swap, o.y, keep * a.y));
+            const V o = theirs[i ^ (uint64_t{1} << t)];
+            a = V{fma(swap, o.x, keep * a.x), fma(swap, o.y, keep * a.y)};
         }
         mine[i] = a;
     }
@@ -334,8 +355,11 @@ __device__ __forceinline__ DD block_reduce(DD v) {
 // probability), four independent 16 B loads per thread per iteration (one
 // in flight per thread left HBM at 4.4 TB/s), compensated per thread, then
 // merged in a fixed order (deterministic).
+// Single-precision registers widen each amplitude to double before squaring
+// (AmpVector::norm_squared, register.cpp:62-73).
+template <class V>
 __global__ void __launch_bounds__(kReduceThreads)
-k_reduce_norm(const double2* __restrict__ amps, uint64_t len, uint64_t goff, int t,
+k_reduce_norm(const V* __restrict__ amps, uint64_t len, uint64_t goff, int t,
               int outcome, double2* __restrict__ partials) {
     DD acc{0.0, 0.0};
     int lb = 0;
@@ -350,20 +374,24 @@ k_reduce_norm(const double2* __restrict__ amps, uint64_t len, uint64_t goff, int
         return ((k >> t) << (t + 1)) | (static_cast<uint64_t>(outcome) << t) | low;
     };
     for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n; k += 4 * stride) {
-        double2 v[4];
+        V v[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const uint64_t kk = k + u * stride;
-            v[u] = kk < n ? __ldcs(amps + at(kk)) : make_double2(0.0, 0.0);
+            v[u] = kk < n ? __ldcs(amps + at(kk)) : V{0, 0};
         }
 #pragma unroll
-        for (int u = 0; u < 4; ++u) dd_acc(acc, __dadd_rn(__dmul_rn(v[u].x, v[u].x), __dmul_rn(v[u].y, v[u].y)));
+        for (int u = 0; u < 4; ++u) {
+            const double x = v[u].x, y = v[u].y;
+            dd_acc(acc, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
+        }
     }
     acc = block_reduce(acc);
     if (threadIdx.x == 0) partials[blockIdx.x] = make_double2(acc.hi, acc.lo);
 }
 
-__global__ void k_reduce_diag(const double2* __restrict__ amps, uint64_t len, uint64_t goff,
+template <class V>
+__global__ void k_reduce_diag(const V* __restrict__ amps, uint64_t len, uint64_t goff,
                               int N, int t, int outcome, int comp, double2* __restrict__ partials) {
     DD acc{0.0, 0.0};
     const uint64_t dim = uint64_t{1} << N;
@@ -372,7 +400,7 @@ __global__ void k_reduce_diag(const double2* __restrict__ amps, uint64_t len, ui
         const uint64_t g = j * (dim + 1);
         if (g < goff || g >= goff + len) continue;
         if (t >= 0 && static_cast<int>((j >> t) & 1u) != outcome) continue;
-        dd_acc(acc, comp ? amps[g - goff].y : amps[g - goff].x);
+        dd_acc(acc, static_cast<double>(comp ? amps[g - goff].y : amps[g - goff].x));
     }
     acc = block_reduce(acc);
     if (threadIdx.x == 0) partials[blockIdx.x] = make_double2(acc.hi, acc.lo);
@@ -387,7 +415,8 @@ __global__ void k_reduce_final(const double2* __restrict__ partials, int n,
     if (threadIdx.x == 0) *result = make_double2(acc.hi, acc.lo);
 }
 
-__global__ void k_fill(double2* __restrict__ amps, uint64_t len, double2 value) {
+template <class V>
+__global__ void k_fill(V* __restrict__ amps, uint64_t len, V value) {
     for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < len;
          i += static_cast<uint64_t>(gridDim.x) * blockDim.x)
         amps[i] = value;
@@ -414,84 +443,146 @@ void launch_pass(double2* amps, const PassParams& p, cudaStream_t s) {
     count_launch();
 }
 
-void launch_gate_simple(double2* amps, int local_qubits, int target, uint64_t cmask,
-                        const Mat2& m, int cls, cudaStream_t s) {
+namespace {
+
+template <class V, class R>
+void gate_simple(V* amps, int local_qubits, int target, uint64_t cmask, const Mat2& mat, int cls,
+                 cudaStream_t s) {
     const uint64_t pairs = uint64_t{1} << (local_qubits - 1);
     const unsigned g = grid_for(pairs, 256);
+    const MatT<R> m = narrow<R>(mat);
     switch (cls) {
     case CLS_REAL: k_gate_simple<CLS_REAL><<<g, 256, 0, s>>>(amps, pairs, target, cmask, m); break;
     case CLS_RX: k_gate_simple<CLS_RX><<<g, 256, 0, s>>>(amps, pairs, target, cmask, m); break;
     case CLS_SWAP: k_gate_simple<CLS_SWAP><<<g, 256, 0, s>>>(amps, pairs, target, cmask, m); break;
     default: k_gate_simple<CLS_GENERIC><<<g, 256, 0, s>>>(amps, pairs, target, cmask, m); break;
     }
-    count_launch();
 }
 
-void launch_diag_simple(double2* amps, uint64_t len, uint64_t goff, int target, uint64_t cmask,
-                        const Mat2& m, uint8_t flags, cudaStream_t s) {
-    k_diag_simple<<<grid_for(len, 256), 256, 0, s>>>(amps, len, goff, target, cmask, m, flags);
-    count_launch();
-}
-
-void launch_dephase(double2* amps, uint64_t len, uint64_t goff, int q0, int q1, double scale,
-                    cudaStream_t s) {
-    k_dephase<<<grid_for(len, 256), 256, 0, s>>>(amps, len, goff, q0, q1, scale);
-    count_launch();
-}
-
-void launch_collapse(double2* amps, uint64_t len, uint64_t goff, int q0, int q1, int outcome,
-                     double scale, cudaStream_t s) {
-    k_collapse<<<grid_for(len, 256), 256, 0, s>>>(amps, len, goff, q0, q1, outcome, scale);
-    count_launch();
-}
-
-void launch_depolarise(double2* amps, int local_qubits, int t, int tN, double keep, double swap,
-                       double off, cudaStream_t s) {
-    const uint64_t count = uint64_t{1} << (local_qubits - 2);
-    k_depolarise<<<grid_for(count, 256), 256, 0, s>>>(amps, count, t, tN, keep, swap, off);
-    count_launch();
-}
-
-void launch_combine(double2* mine, const double2* theirs, uint64_t len, uint64_t idx0,
-                    uint64_t low_mask, int own_lo, const Mat2& m, int cls, cudaStream_t s) {
+template <class V, class R>
+void combine(V* mine, const V* theirs, uint64_t len, uint64_t idx0, uint64_t low_mask, int own_lo,
+             const Mat2& mat, int cls, cudaStream_t s) {
     const unsigned g = grid_for(len, 256);
+    const MatT<R> m = narrow<R>(mat);
     switch (cls) {
     case CLS_REAL: k_combine<CLS_REAL><<<g, 256, 0, s>>>(mine, theirs, len, idx0, low_mask, own_lo, m); break;
     case CLS_RX: k_combine<CLS_RX><<<g, 256, 0, s>>>(mine, theirs, len, idx0, low_mask, own_lo, m); break;
     case CLS_SWAP: k_combine<CLS_SWAP><<<g, 256, 0, s>>>(mine, theirs, len, idx0, low_mask, own_lo, m); break;
     default: k_combine<CLS_GENERIC><<<g, 256, 0, s>>>(mine, theirs, len, idx0, low_mask, own_lo, m); break;
     }
+}
+
+template <class V> V* as(void* p) { return static_cast<V*>(p); }
+template <class V> const V* as(const void* p) { return static_cast<const V*>(p); }
+
+} // namespace
+
+void launch_gate_simple(void* amps, bool single, int local_qubits, int target, uint64_t cmask,
+                        const Mat2& m, int cls, cudaStream_t s) {
+    if (single)
+        gate_simple<float2, float>(as<float2>(amps), local_qubits, target, cmask, m, cls, s);
+    else
+        gate_simple<double2, double>(as<double2>(amps), local_qubits, target, cmask, m, cls, s);
     count_launch();
 }
 
-void launch_combine_depol(double2* mine, const double2* theirs, uint64_t len, uint64_t idx0,
+void launch_diag_simple(void* amps, bool single, uint64_t len, uint64_t goff, int target,
+                        uint64_t cmask, const Mat2& m, uint8_t flags, cudaStream_t s) {
+    const unsigned g = grid_for(len, 256);
+    if (single)
+        k_diag_simple<<<g, 256, 0, s>>>(as<float2>(amps), len, goff, target, cmask, narrow<float>(m), flags);
+    else
+        k_diag_simple<<<g, 256, 0, s>>>(as<double2>(amps), len, goff, target, cmask, narrow<double>(m), flags);
+    count_launch();
+}
+
+void launch_dephase(void* amps, bool single, uint64_t len, uint64_t goff, int q0, int q1,
+                    double scale, cudaStream_t s) {
+    const unsigned g = grid_for(len, 256);
+    if (single)
+        k_dephase<<<g, 256, 0, s>>>(as<float2>(amps), len, goff, q0, q1, static_cast<float>(scale));
+    else
+        k_dephase<<<g, 256, 0, s>>>(as<double2>(amps), len, goff, q0, q1, scale);
+    count_launch();
+}
+
+void launch_collapse(void* amps, bool single, uint64_t len, uint64_t goff, int q0, int q1,
+                     int outcome, double scale, cudaStream_t s) {
+    const unsigned g = grid_for(len, 256);
+    if (single)
+        k_collapse<<<g, 256, 0, s>>>(as<float2>(amps), len, goff, q0, q1, outcome, static_cast<float>(scale));
+    else
+        k_collapse<<<g, 256, 0, s>>>(as<double2>(amps), len, goff, q0, q1, outcome, scale);
+    count_launch();
+}
+
+void launch_depolarise(void* amps, bool single, int local_qubits, int t, int tN, double keep,
+                       double swap, double off, cudaStream_t s) {
+    const uint64_t count = uint64_t{1} << (local_qubits - 2);
+    const unsigned g = grid_for(count, 256);
+    if (single)
+        k_depolarise<<<g, 256, 0, s>>>(as<float2>(amps), count, t, tN, static_cast<float>(keep),
+                                       static_cast<float>(swap), static_cast<float>(off));
+    else
+        k_depolarise<<<g, 256, 0, s>>>(as<double2>(amps), count, t, tN, keep, swap, off);
+    count_launch();
+}
+
+void launch_combine(void* mine, const void* theirs, bool single, uint64_t len, uint64_t idx0,
+                    uint64_t low_mask, int own_lo, const Mat2& m, int cls, cudaStream_t s) {
+    if (single)
+        combine<float2, float>(as<float2>(mine), as<float2>(theirs), len, idx0, low_mask, own_lo, m, cls, s);
+    else
+        combine<double2, double>(as<double2>(mine), as<double2>(theirs), len, idx0, low_mask, own_lo, m, cls, s);
+    count_launch();
+}
+
+void launch_combine_depol(void* mine, const void* theirs, bool single, uint64_t len, uint64_t idx0,
                           int t, int own_col, double keep, double swap, double off,
                           cudaStream_t s) {
-    k_combine_depol<<<grid_for(len, 256), 256, 0, s>>>(mine, theirs, len, idx0, t, own_col, keep,
-                                                      swap, off);
+    const unsigned g = grid_for(len, 256);
+    if (single)
+        k_combine_depol<<<g, 256, 0, s>>>(as<float2>(mine), as<float2>(theirs), len, idx0, t, own_col,
+                                          static_cast<float>(keep), static_cast<float>(swap),
+                                          static_cast<float>(off));
+    else
+        k_combine_depol<<<g, 256, 0, s>>>(as<double2>(mine), as<double2>(theirs), len, idx0, t, own_col,
+                                          keep, swap, off);
     count_launch();
 }
 
-void launch_reduce_norm(const double2* amps, uint64_t len, uint64_t goff, int t, int outcome,
-                        double2* partials, double2* result, cudaStream_t s) {
-    k_reduce_norm<<<kReduceBlocks, kReduceThreads, 0, s>>>(amps, len, goff, t, outcome, partials);
+void launch_reduce_norm(const void* amps, bool single, uint64_t len, uint64_t goff, int t,
+                        int outcome, double2* partials, double2* result, cudaStream_t s) {
+    if (single)
+        k_reduce_norm<<<kReduceBlocks, kReduceThreads, 0, s>>>(as<float2>(amps), len, goff, t, outcome, partials);
+    else
+        k_reduce_norm<<<kReduceBlocks, kReduceThreads, 0, s>>>(as<double2>(amps), len, goff, t, outcome, partials);
     k_reduce_final<<<1, kReduceThreads, 0, s>>>(partials, kReduceBlocks, result);
     count_launch();
     count_launch();
 }
 
-void launch_reduce_diag(const double2* amps, uint64_t len, uint64_t goff, int N, int t,
+void launch_reduce_diag(const void* amps, bool single, uint64_t len, uint64_t goff, int N, int t,
                         int outcome, int comp, double2* partials, double2* result,
                         cudaStream_t s) {
-    k_reduce_diag<<<kReduceBlocks, kReduceThreads, 0, s>>>(amps, len, goff, N, t, outcome, comp,
-                                                          partials);
+    if (single)
+        k_reduce_diag<<<kReduceBlocks, kReduceThreads, 0, s>>>(as<float2>(amps), len, goff, N, t, outcome,
+                                                              comp, partials);
+    else
+        k_reduce_diag<<<kReduceBlocks, kReduceThreads, 0, s>>>(as<double2>(amps), len, goff, N, t, outcome,
+                                                              comp, partials);
     k_reduce_final<<<1, kReduceThreads, 0, s>>>(partials, kReduceBlocks, result);
     count_launch();
     count_launch();
 }
 
-void launch_fill(double2* amps, uint64_t len, double2 value, cudaStream_t s) {
-    k_fill<<<grid_for(len, 256), 256, 0, s>>>(amps, len, value);
+void launch_fill(void* amps, bool single, uint64_t len, double re, double im, cudaStream_t s) {
+    const unsigned g = grid_for(len, 256);
+    if (single)
+        k_fill<<<g, 256, 0, s>>>(as<float2>(amps), len,
+                                 make_float2(static_cast<float>(re), static_cast<float>(im)));
+    else
+        k_fill<<<g, 256, 0, s>>>(as<double2>(amps), len, make_double2(re, im));
     count_launch();
 }
 

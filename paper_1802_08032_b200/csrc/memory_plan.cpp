@@ -65,17 +65,18 @@ int max_qubits(uint64_t node_bytes, uint64_t overhead, int strategy, bool single
     return best;
 }
 
-uint64_t device_bytes_per_rank(int flat, int k, uint64_t chunk_amps) {
+uint64_t device_bytes_per_rank(int flat, int k, uint64_t chunk_amps, bool single) {
     if (flat < 1 || k < 0 || k > flat || flat - k > 58)
         throw DomainError("invalid qubit/rank combination");
     const uint64_t local = uint64_t{1} << (flat - k);
-    uint64_t bytes = local * sizeof(double2);
-    if (k > 0) bytes += 2 * std::min(local, std::max<uint64_t>(chunk_amps, 1)) * sizeof(double2);
+    const uint64_t amp = single ? sizeof(float2) : sizeof(double2);
+    uint64_t bytes = local * amp;
+    if (k > 0) bytes += 2 * std::min(local, std::max<uint64_t>(chunk_amps, 1)) * amp;
     bytes += (kReduceBlocks + (uint64_t{1} << k) + 1) * sizeof(double2);
     return bytes;
 }
 
-int device_max_qubits(uint64_t device_bytes, int k, uint64_t chunk_amps, bool density) {
+int device_max_qubits(uint64_t device_bytes, int k, uint64_t chunk_amps, bool density, bool single) {
     if (k < 0 || k > 30) throw DomainError("rank count exponent must be in [0, 30]");
     int best = 0;
     for (int N = 1; N <= 58; ++N) {
@@ -85,7 +86,7 @@ int device_max_qubits(uint64_t device_bytes, int k, uint64_t chunk_amps, bool de
             continue;
         }
         if (density && k > N) continue;
-        if (device_bytes_per_rank(flat, k, chunk_amps) <= device_bytes)
+        if (device_bytes_per_rank(flat, k, chunk_amps, single) <= device_bytes)
             best = N;
         else
             break;

@@ -34,11 +34,10 @@ __device__ __forceinline__ uint64_t pair_base_index(uint64_t i, int t) {
 
 // One output row of the pair update; Z = coefficients known to be zero
 // (bit0 q0, bit1 q1, bit2 q2, bit3 q3).
-template <int Z>
-__device__ __forceinline__ double2 row(double q0, double q1, double q2, double q3,
-                                       double2 lo, double2 hi) {
+template <int Z, class R, class V>
+__device__ __forceinline__ V row(R q0, R q1, R q2, R q3, V lo, V hi) {
     constexpr bool n0 = !(Z & 1), n1 = !(Z & 2), n2 = !(Z & 4), n3 = !(Z & 8);
-    double re, im;
+    R re, im;
     if constexpr (n0 && n1) {
         re = fma(q0, lo.x, -(q1 * lo.y));
         im = fma(q0, lo.y, q1 * lo.x);
@@ -49,8 +48,8 @@ __device__ __forceinline__ double2 row(double q0, double q1, double q2, double q
         re = -(q1 * lo.y);
         im = q1 * lo.x;
     } else {
-        re = 0.0;
-        im = 0.0;
+        re = R(0);
+        im = R(0);
     }
     if constexpr (n2) {
         re = fma(q2, hi.x, re);
@@ -61,7 +60,7 @@ __device__ __forceinline__ double2 row(double q0, double q1, double q2, double q
                                  // the register operand so q3 can be a constant-bank one
         im = fma(q3, hi.x, im);
     }
-    return make_double2(re, im);
+    return V{re, im};
 }
 
 // Zero patterns of the two rows per class (see GateClass in qgpu_device.h).
@@ -70,14 +69,14 @@ template <> struct ClassZ<CLS_GENERIC> { static constexpr int z0 = 0, z1 = 0; };
 template <> struct ClassZ<CLS_REAL> { static constexpr int z0 = 0b1010, z1 = 0b1010; };
 template <> struct ClassZ<CLS_RX> { static constexpr int z0 = 0b0110, z1 = 0b1001; };
 
-template <int CLS>
-__device__ __forceinline__ void pair_update(double2& lo, double2& hi, const double* m) {
+template <int CLS, class V, class R>
+__device__ __forceinline__ void pair_update(V& lo, V& hi, const R* m) {
     if constexpr (CLS == CLS_SWAP) {
-        const double2 t = lo;
+        const V t = lo;
         lo = hi;
         hi = t;
     } else {
-        const double2 l = lo, h = hi;
+        const V l = lo, h = hi;
         lo = row<ClassZ<CLS>::z0>(m[0], m[1], m[2], m[3], l, h);
         hi = row<ClassZ<CLS>::z1>(m[4], m[5], m[6], m[7], l, h);
     }
@@ -87,13 +86,14 @@ __device__ __forceinline__ void pair_update(double2& lo, double2& hi, const doub
 // d * v (b = 1), each with the rounding of its reference row (the a term is
 // the fused first product of the low row; the d term is the second product of
 // the high row, so it rounds the other way round).
-__device__ __forceinline__ double2 diag_mul(const double* m, uint32_t b, double2 v) {
-    const double ar = m[0], ai = m[1], dr = m[6], di = m[7];
-    const double s1 = b ? -di : ar, t1 = b ? v.y : v.x;
-    const double s2 = b ? dr : -ai, t2 = b ? v.x : v.y;
-    const double u1 = b ? di : ar, w1 = b ? v.x : v.y;
-    const double u2 = b ? dr : ai, w2 = b ? v.y : v.x;
-    return make_double2(fma(s1, t1, s2 * t2), fma(u1, w1, u2 * w2));
+template <class R, class V>
+__device__ __forceinline__ V diag_mul(const R* m, uint32_t b, V v) {
+    const R ar = m[0], ai = m[1], dr = m[6], di = m[7];
+    const R s1 = b ? -di : ar, t1 = b ? v.y : v.x;
+    const R s2 = b ? dr : -ai, t2 = b ? v.x : v.y;
+    const R u1 = b ? di : ar, w1 = b ? v.x : v.y;
+    const R u2 = b ? dr : ai, w2 = b ? v.y : v.x;
+    return V{fma(s1, t1, s2 * t2), fma(u1, w1, u2 * w2)};
 }
 
 } // namespace qgpu

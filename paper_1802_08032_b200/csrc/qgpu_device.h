@@ -198,6 +198,7 @@ struct TileParams {
     int32_t high_pos[kTileHigh];           // global qubits of tile bits 5.. (any order)
     int32_t high_sorted[kTileHigh];        // the same qubits, ascending
     int32_t any_outer;                     // some op has controls outside the tile
+    int32_t single;                        // amplitudes are float2 (else double2)
     uint64_t seg_off[1 << kTileHigh];      // global offset of tile segment s
     // the last phase stores straight to HBM: local-index offsets of its
     // register i, warp w and lane bits 3, 4 (lane bits 0-2: qubits 0-2)

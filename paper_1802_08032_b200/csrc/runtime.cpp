@@ -106,7 +106,7 @@ int plan_gate(int flat, int rank_log2, int rank, int target, uint64_t cmask, int
 
 // ---------------------------------------------------------------- register
 
-QuregImpl* create_register(Env* env, int N, bool density) {
+QuregImpl* create_register(Env* env, int N, bool density, bool single) {
     if (N < 1)
         throw DomainError("register needs at least 1 qubit, got " + std::to_string(N));
     const int flat = density ? 2 * N : N;
@@ -127,10 +127,10 @@ QuregImpl* create_register(Env* env, int N, bool density) {
         size_t free_b = 0, total_b = 0;
         if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
             const int nsh = env->mode == Mode::Loopback ? env->num_ranks : 1;
-            const uint64_t per = device_bytes_per_rank(flat, env->rank_log2, env->chunk_amps);
+            const uint64_t per = device_bytes_per_rank(flat, env->rank_log2, env->chunk_amps, single);
             const unsigned __int128 need = static_cast<unsigned __int128>(per) * nsh;
             if (need > free_b) {
-                const int mq = device_max_qubits(free_b / nsh, env->rank_log2, env->chunk_amps, density);
+                const int mq = device_max_qubits(free_b / nsh, env->rank_log2, env->chunk_amps, density, single);
                 throw ResourceError("register of " + std::to_string(N) + " qubits needs " +
                                     std::to_string(per) + " bytes per rank but " +
                                     std::to_string(free_b) + " bytes of device memory are free: " +
@@ -146,10 +146,11 @@ QuregImpl* create_register(Env* env, int N, bool density) {
     q->N = N;
     q->flat = flat;
     q->density = density;
+    q->single = single;
     q->local_qubits = flat - env->rank_log2;
     q->local_len = uint64_t{1} << q->local_qubits;
     const int nshards = env->mode == Mode::Loopback ? env->num_ranks : 1;
-    const size_t bytes = q->local_len * sizeof(double2);
+    const size_t bytes = q->local_len * q->amp_bytes();
     for (int s = 0; s < nshards; ++s) {
         Shard sh;
         sh.rank = env->mode == Mode::Loopback ? s : env->rank;
@@ -170,8 +171,9 @@ QuregImpl* create_register(Env* env, int N, bool density) {
     q->fill_zero();
     if (q->shards[0].rank == 0) {
         const double2 one = make_double2(1.0, 0.0);
-        cuda_check(cudaMemcpyAsync(q->shards[0].amps, &one, sizeof(one), cudaMemcpyHostToDevice,
-                                   env->stream),
+        const float2 one_f = make_float2(1.0f, 0.0f);
+        cuda_check(cudaMemcpyAsync(q->shards[0].amps, single ? static_cast<const void*>(&one_f) : &one,
+                                   q->amp_bytes(), cudaMemcpyHostToDevice, env->stream),
                    "init zero state");
         cuda_check(cudaStreamSynchronize(env->stream), "init zero state");
     }
@@ -194,7 +196,7 @@ QuregImpl::~QuregImpl() {
 void QuregImpl::fill_zero() {
     discard_all();
     for (auto& s : shards)
-        cuda_check(cudaMemsetAsync(s.amps, 0, local_len * sizeof(double2), env->stream),
+        cuda_check(cudaMemsetAsync(s.amps, 0, local_len * amp_bytes(), env->stream),
                    "cudaMemsetAsync");
     sp.reset(flat, local_qubits, env->chunk_amps); // the whole state is rewritten
 }
@@ -206,10 +208,10 @@ void QuregImpl::ensure_recv(uint64_t len) {
     cudaFree(recv[1]);
     recv[0] = recv[1] = nullptr;
     recv_len = 0;
-    if (cudaMalloc(&recv[0], len * sizeof(double2)) != cudaSuccess ||
-        cudaMalloc(&recv[1], len * sizeof(double2)) != cudaSuccess) {
+    if (cudaMalloc(&recv[0], len * amp_bytes()) != cudaSuccess ||
+        cudaMalloc(&recv[1], len * amp_bytes()) != cudaSuccess) {
         cudaGetLastError();
-        throw ResourceError("failed to allocate " + std::to_string(2 * len * sizeof(double2)) +
+        throw ResourceError("failed to allocate " + std::to_string(2 * len * amp_bytes()) +
                             " bytes of exchange buffers");
     }
     recv_len = len;
@@ -366,7 +368,9 @@ void QuregImpl::enqueue_phys(const FlatOp& op) {
         run_exchange_gate(op);
         return;
     }
-    if (env->fusion_mode == 2 || pass_H() < 1) {
+    // states too small to tile run one kernel per op in single precision (the
+    // register-only small-state pass is instantiated for double only)
+    if (env->fusion_mode == 2 || pass_H() < 1 || (single && !use_tile())) {
         flush_pass();
         run_simple(op);
         ++passes;
@@ -459,6 +463,7 @@ void QuregImpl::launch_tile() {
     TileParams P;
     std::memset(&P, 0, sizeof(P));
     P.num_tiles = uint64_t{1} << (local_qubits - kTileQubits);
+    P.single = single ? 1 : 0;
     P.num_phases = static_cast<int>(phases.size());
     for (int j = 0; j < kTileHigh; ++j) P.high_pos[j] = high[j];
     for (int s = 0; s < (1 << kTileHigh); ++s) {
@@ -845,7 +850,7 @@ void QuregImpl::launch_fused() {
     ProfScope prof(env, PK_PASS);
     for (auto& s : shards) {
         P.global_offset = goff(s);
-        launch_pass(s.amps, P, env->stream);
+        launch_pass(static_cast<double2*>(s.amps), P, env->stream); // double only (see enqueue_phys)
     }
     cuda_check(cudaGetLastError(), "fused pass launch");
     ++passes;
@@ -859,22 +864,22 @@ void QuregImpl::run_simple(const FlatOp& op) {
             if (op.cls == CLS_DIAG) {
                 Mat2 m;
                 std::memcpy(m.m, op.m, sizeof(m.m));
-                launch_diag_simple(s.amps, local_len, goff(s), op.q0, op.cmask, m, op.flags,
+                launch_diag_simple(s.amps, single, local_len, goff(s), op.q0, op.cmask, m, op.flags,
                                    env->stream);
             } else {
                 const uint64_t rank_mask = op.cmask >> local_qubits;
                 if ((static_cast<uint64_t>(s.rank) & rank_mask) != rank_mask) break;
                 Mat2 m;
                 std::memcpy(m.m, op.m, sizeof(m.m));
-                launch_gate_simple(s.amps, local_qubits, op.q0, op.cmask & (local_len - 1), m,
+                launch_gate_simple(s.amps, single, local_qubits, op.q0, op.cmask & (local_len - 1), m,
                                    op.cls, env->stream);
             }
             break;
         case FK_DEPHASE:
-            launch_dephase(s.amps, local_len, goff(s), op.q0, op.q1, op.m[0], env->stream);
+            launch_dephase(s.amps, single, local_len, goff(s), op.q0, op.q1, op.m[0], env->stream);
             break;
         case FK_COLLAPSE:
-            launch_collapse(s.amps, local_len, goff(s), op.q0, op.q1, op.outcome, op.m[0],
+            launch_collapse(s.amps, single, local_len, goff(s), op.q0, op.q1, op.outcome, op.m[0],
                             env->stream);
             break;
         default: break;
@@ -915,7 +920,7 @@ template <class Combine>
 static void exchange_rounds(QuregImpl& q, int rank_bit, uint64_t rank_mask, uint64_t chunk,
                             Combine&& combine) {
     Env* env = q.env;
-    const uint64_t bytes = chunk * sizeof(double2);
+    const uint64_t bytes = chunk * q.amp_bytes();
     if (env->mode == Mode::Nccl) {
         Shard& s = q.shards[0];
         if ((static_cast<uint64_t>(s.rank) & rank_mask) != rank_mask) return;
@@ -927,10 +932,10 @@ static void exchange_rounds(QuregImpl& q, int rank_bit, uint64_t rank_mask, uint
         for (uint64_t c0 = 0; c0 < q.local_len; c0 += chunk, ++j) {
             const int b = static_cast<int>(j & 1);
             if (j >= 2) cuda_check(cudaStreamWaitEvent(env->comm_stream, ev.done[b], 0), "event");
-            env->nccl->sendrecv(peer, s.amps + c0, q.recv[b], bytes, env->comm_stream);
+            env->nccl->sendrecv(peer, q.at(s.amps, c0), q.recv[b], bytes, env->comm_stream);
             cuda_check(cudaEventRecord(ev.recv[b], env->comm_stream), "event");
             cuda_check(cudaStreamWaitEvent(env->stream, ev.recv[b], 0), "event");
-            combine(s, s.amps + c0, q.recv[b], chunk, c0);
+            combine(s, q.at(s.amps, c0), q.recv[b], chunk, c0);
             cuda_check(cudaEventRecord(ev.done[b], env->stream), "event");
             s.messages += 1;
             s.bytes += bytes;
@@ -947,14 +952,14 @@ static void exchange_rounds(QuregImpl& q, int rank_bit, uint64_t rank_mask, uint
         if ((static_cast<uint64_t>(s.rank) & rank_mask) != rank_mask) continue;
         Shard& p = q.shards[peer];
         for (uint64_t c0 = 0; c0 < q.local_len; c0 += chunk) {
-            cuda_check(cudaMemcpyAsync(q.recv[0], p.amps + c0, bytes, cudaMemcpyDeviceToDevice,
+            cuda_check(cudaMemcpyAsync(q.recv[0], q.at(p.amps, c0), bytes, cudaMemcpyDeviceToDevice,
                                        env->stream),
                        "loopback exchange");
-            cuda_check(cudaMemcpyAsync(q.recv[1], s.amps + c0, bytes, cudaMemcpyDeviceToDevice,
+            cuda_check(cudaMemcpyAsync(q.recv[1], q.at(s.amps, c0), bytes, cudaMemcpyDeviceToDevice,
                                        env->stream),
                        "loopback exchange");
-            combine(s, s.amps + c0, q.recv[0], chunk, c0);
-            combine(p, p.amps + c0, q.recv[1], chunk, c0);
+            combine(s, q.at(s.amps, c0), q.recv[0], chunk, c0);
+            combine(p, q.at(p.amps, c0), q.recv[1], chunk, c0);
             s.messages += 1;
             s.bytes += bytes;
             p.messages += 1;
@@ -973,9 +978,9 @@ void QuregImpl::run_exchange_gate(const FlatOp& op) {
     std::memcpy(m.m, op.m, sizeof(m.m));
     ProfScope prof(env, PK_EXCHANGE);
     exchange_rounds(*this, rank_bit, rank_mask, chunk,
-                    [&](Shard& s, double2* mine, double2* theirs, uint64_t len, uint64_t idx0) {
+                    [&](Shard& s, void* mine, void* theirs, uint64_t len, uint64_t idx0) {
                         const int own_lo = ((s.rank >> rank_bit) & 1) == 0;
-                        launch_combine(mine, theirs, len, idx0, low_mask, own_lo, m, op.cls,
+                        launch_combine(mine, theirs, single, len, idx0, low_mask, own_lo, m, op.cls,
                                        env->stream);
                     });
     cuda_check(cudaGetLastError(), "exchange combine");
@@ -987,7 +992,7 @@ void QuregImpl::run_depol(const FlatOp& op) {
     ProfScope prof(env, PK_DEPOL);
     if (op.q1 < local_qubits) {
         for (auto& s : shards)
-            launch_depolarise(s.amps, local_qubits, op.q0, op.q1, keep, swap, off, env->stream);
+            launch_depolarise(s.amps, single, local_qubits, op.q0, op.q1, keep, swap, off, env->stream);
         cuda_check(cudaGetLastError(), "depolarise");
         ++passes;
         return;
@@ -997,9 +1002,9 @@ void QuregImpl::run_depol(const FlatOp& op) {
     chunk = std::max<uint64_t>(chunk, uint64_t{2} << op.q0);
     ensure_recv(chunk);
     exchange_rounds(*this, rank_bit, 0, chunk,
-                    [&](Shard& s, double2* mine, double2* theirs, uint64_t len, uint64_t idx0) {
+                    [&](Shard& s, void* mine, void* theirs, uint64_t len, uint64_t idx0) {
                         const int own_col = (s.rank >> rank_bit) & 1;
-                        launch_combine_depol(mine, theirs, len, idx0, op.q0, own_col, keep, swap,
+                        launch_combine_depol(mine, theirs, single, len, idx0, op.q0, own_col, keep, swap,
                                              off, env->stream);
                     });
     cuda_check(cudaGetLastError(), "depolarise exchange");
@@ -1021,7 +1026,7 @@ void QuregImpl::run_swap(int g, int v) {
     const uint64_t unit = std::min<uint64_t>(std::min<uint64_t>(env->chunk_amps, block), local_len / 2);
     const uint64_t units = (local_len / 2) / unit;
     ensure_recv(unit);
-    const uint64_t bytes = unit * sizeof(double2);
+    const uint64_t bytes = unit * amp_bytes();
     // offset of the u-th unit of the half whose bit v == side
     auto offset = [&](uint64_t u, int side) {
         const uint64_t e = u * unit;                      // element index within the half
@@ -1038,7 +1043,7 @@ void QuregImpl::run_swap(int g, int v) {
         cuda_check(cudaStreamWaitEvent(env->comm_stream, ev.start, 0), "event");
         for (uint64_t u = 0; u < units; ++u) {
             const int b = static_cast<int>(u & 1);
-            double2* mine = s.amps + offset(u, a ^ 1);
+            void* mine = at(s.amps, offset(u, a ^ 1));
             if (u >= 2) cuda_check(cudaStreamWaitEvent(env->comm_stream, ev.done[b], 0), "event");
             env->nccl->sendrecv(peer, mine, recv[b], bytes, env->comm_stream);
             cuda_check(cudaEventRecord(ev.recv[b], env->comm_stream), "event");
@@ -1056,8 +1061,8 @@ void QuregImpl::run_swap(int g, int v) {
             Shard& p = shards[peer];
             // s has bit j = 0 (trades its bit-v = 1 half), p has bit j = 1
             for (uint64_t u = 0; u < units; ++u) {
-                double2* x = s.amps + offset(u, 1);
-                double2* y = p.amps + offset(u, 0);
+                void* x = at(s.amps, offset(u, 1));
+                void* y = at(p.amps, offset(u, 0));
                 cuda_check(cudaMemcpyAsync(recv[0], x, bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
                 cuda_check(cudaMemcpyAsync(x, y, bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
                 cuda_check(cudaMemcpyAsync(y, recv[0], bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
@@ -1152,7 +1157,7 @@ double QuregImpl::reduce_norm(int t, int outcome) {
     if (swaps_on()) t = sp.phys(t);
     ProfScope prof(env, PK_REDUCE);
     for (size_t k = 0; k < shards.size(); ++k)
-        launch_reduce_norm(shards[k].amps, local_len, goff(shards[k]), t, outcome, partials,
+        launch_reduce_norm(shards[k].amps, single, local_len, goff(shards[k]), t, outcome, partials,
                            results + k, env->stream);
     cuda_check(cudaGetLastError(), "reduce");
     return combine_results(static_cast<int>(shards.size()));
@@ -1163,7 +1168,7 @@ double QuregImpl::reduce_diag(int t, int outcome, int comp) {
     flush();
     ProfScope prof(env, PK_REDUCE);
     for (size_t k = 0; k < shards.size(); ++k)
-        launch_reduce_diag(shards[k].amps, local_len, goff(shards[k]), N, t, outcome, comp,
+        launch_reduce_diag(shards[k].amps, single, local_len, goff(shards[k]), N, t, outcome, comp,
                            partials, results + k, env->stream);
     cuda_check(cudaGetLastError(), "reduce");
     return combine_results(static_cast<int>(shards.size()));
@@ -1177,7 +1182,7 @@ Complex QuregImpl::trace() {
     return c;
 }
 
-void QuregImpl::get_flat(uint64_t start, uint64_t num, double2* out) {
+void QuregImpl::get_raw(uint64_t start, uint64_t num, void* out) {
     restore_identity();
     flush();
     const uint64_t end = start + num;
@@ -1187,7 +1192,7 @@ void QuregImpl::get_flat(uint64_t start, uint64_t num, double2* out) {
             if (start < lo || end > hi)
                 throw DomainError("bulk reads are limited to this rank's amplitudes [" +
                                   std::to_string(lo) + ", " + std::to_string(hi) + ")");
-            cuda_check(cudaMemcpyAsync(out, shards[0].amps + (start - lo), num * sizeof(double2),
+            cuda_check(cudaMemcpyAsync(out, at(shards[0].amps, start - lo), num * amp_bytes(),
                                        cudaMemcpyDeviceToHost, env->stream),
                        "read");
             cuda_check(cudaStreamSynchronize(env->stream), "read");
@@ -1198,7 +1203,7 @@ void QuregImpl::get_flat(uint64_t start, uint64_t num, double2* out) {
         const int owner = static_cast<int>(start >> local_qubits);
         double2 zero = make_double2(0.0, 0.0);
         if (owner == shards[0].rank)
-            cuda_check(cudaMemcpyAsync(results, shards[0].amps + (start - lo), sizeof(double2),
+            cuda_check(cudaMemcpyAsync(results, at(shards[0].amps, start - lo), amp_bytes(),
                                        cudaMemcpyDeviceToDevice, env->stream),
                        "read");
         else
@@ -1206,7 +1211,7 @@ void QuregImpl::get_flat(uint64_t start, uint64_t num, double2* out) {
                                        env->stream),
                        "read");
         env->nccl->allgather(results, results + 1, sizeof(double2), env->stream);
-        cuda_check(cudaMemcpyAsync(out, results + 1 + owner, sizeof(double2),
+        cuda_check(cudaMemcpyAsync(out, results + 1 + owner, amp_bytes(),
                                    cudaMemcpyDeviceToHost, env->stream),
                    "read");
         cuda_check(cudaStreamSynchronize(env->stream), "read");
@@ -1216,14 +1221,14 @@ void QuregImpl::get_flat(uint64_t start, uint64_t num, double2* out) {
         const uint64_t lo = goff(s), hi = lo + local_len;
         const uint64_t a = std::max(lo, start), b = std::min(hi, end);
         if (a >= b) continue;
-        cuda_check(cudaMemcpyAsync(out + (a - start), s.amps + (a - lo), (b - a) * sizeof(double2),
+        cuda_check(cudaMemcpyAsync(at(out, a - start), at(s.amps, a - lo), (b - a) * amp_bytes(),
                                    cudaMemcpyDeviceToHost, env->stream),
                    "read");
     }
     cuda_check(cudaStreamSynchronize(env->stream), "read");
 }
 
-void QuregImpl::set_flat(uint64_t start, uint64_t num, const double2* in) {
+void QuregImpl::set_raw(uint64_t start, uint64_t num, const void* in) {
     restore_identity();
     flush();
     const uint64_t end = start + num;
@@ -1231,11 +1236,34 @@ void QuregImpl::set_flat(uint64_t start, uint64_t num, const double2* in) {
         const uint64_t lo = goff(s), hi = lo + local_len;
         const uint64_t a = std::max(lo, start), b = std::min(hi, end);
         if (a >= b) continue;
-        cuda_check(cudaMemcpyAsync(s.amps + (a - lo), in + (a - start), (b - a) * sizeof(double2),
+        cuda_check(cudaMemcpyAsync(at(s.amps, a - lo), at(const_cast<void*>(in), a - start), (b - a) * amp_bytes(),
                                    cudaMemcpyHostToDevice, env->stream),
                    "write");
     }
     cuda_check(cudaStreamSynchronize(env->stream), "write");
+}
+
+// The host boundary is double in both precisions: single-precision registers
+// widen on read and narrow on write (AmpVector::get / set, register.cpp:30-51).
+void QuregImpl::get_flat(uint64_t start, uint64_t num, double2* out) {
+    if (!single) {
+        get_raw(start, num, out);
+        return;
+    }
+    std::vector<float2> tmp(num);
+    get_raw(start, num, tmp.data());
+    for (uint64_t i = 0; i < num; ++i) out[i] = make_double2(tmp[i].x, tmp[i].y);
+}
+
+void QuregImpl::set_flat(uint64_t start, uint64_t num, const double2* in) {
+    if (!single) {
+        set_raw(start, num, in);
+        return;
+    }
+    std::vector<float2> tmp(num);
+    for (uint64_t i = 0; i < num; ++i)
+        tmp[i] = make_float2(static_cast<float>(in[i].x), static_cast<float>(in[i].y));
+    set_raw(start, num, tmp.data());
 }
 
 } // namespace qgpu

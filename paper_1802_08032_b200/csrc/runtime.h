@@ -110,7 +110,7 @@ uint8_t classify(const double* m, uint8_t* diag_flags);
 
 struct Shard {
     int rank = 0;
-    double2* amps = nullptr;
+    void* amps = nullptr; // double2[local_len], or float2[local_len] for single precision
     uint64_t messages = 0, bytes = 0; // CommStats per rank
 };
 
@@ -119,14 +119,19 @@ struct QuregImpl {
     int N = 0;          // qubits represented
     int flat = 0;       // N (SV) or 2N (DM)
     bool density = false;
+    bool single = false; // Precision::Single: float2 amplitudes, float arithmetic
     int local_qubits = 0;
     uint64_t local_len = 0;
     std::vector<Shard> shards; // 1, or 2^k virtual ranks (Loopback)
-    double2* recv[2] = {nullptr, nullptr};
+    void* recv[2] = {nullptr, nullptr};
     uint64_t recv_len = 0;
     double2* partials = nullptr; // reduction scratch
     double2* results = nullptr;  // one (hi, lo) per shard
     uint64_t passes = 0;
+
+    size_t amp_bytes() const { return single ? sizeof(float2) : sizeof(double2); }
+    // element `i` of a shard (or exchange buffer) as a byte address
+    char* at(void* base, uint64_t i) const { return static_cast<char*>(base) + i * amp_bytes(); }
 
     // the open pass
     std::vector<FlatOp> pending;
@@ -191,9 +196,13 @@ struct QuregImpl {
     void ensure_recv(uint64_t len);
     uint64_t goff(const Shard& s) const { return static_cast<uint64_t>(s.rank) * local_len; }
     double combine_results(int n); // rank-ordered double-double sum
+    // amplitude bytes in the register's own precision (get_flat / set_flat
+    // convert at the host boundary)
+    void get_raw(uint64_t start, uint64_t num, void* out);
+    void set_raw(uint64_t start, uint64_t num, const void* in);
 };
 
-QuregImpl* create_register(Env* env, int N, bool density);
+QuregImpl* create_register(Env* env, int N, bool density, bool single = false);
 
 bool pass_stats_enabled();
 void record_pass_stats(const TileParams& P);
@@ -203,8 +212,9 @@ void record_pass_stats(const TileParams& P);
 // this runtime's per-rank device footprint
 uint64_t modeled_bytes_per_rank(int n, int k, int strategy, bool single, uint64_t block);
 int max_qubits(uint64_t node_bytes, uint64_t overhead, int strategy, bool single, int k);
-uint64_t device_bytes_per_rank(int flat, int k, uint64_t chunk_amps);
-int device_max_qubits(uint64_t device_bytes, int k, uint64_t chunk_amps, bool density);
+uint64_t device_bytes_per_rank(int flat, int k, uint64_t chunk_amps, bool single = false);
+int device_max_qubits(uint64_t device_bytes, int k, uint64_t chunk_amps, bool density,
+                      bool single = false);
 
 int plan_gate(int flat, int rank_log2, int rank, int target, uint64_t cmask, int* peer,
               int* own_lo, uint64_t* low_mask);

@@ -17,12 +17,43 @@ namespace {
 template <int RB, int WB, int NBUF>
 __global__ void __launch_bounds__(32 << WB, 1)
 k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
-    tile_pass_body<RB, WB, NBUF, Interp>(amps, P);
+    tile_f64::tile_pass_body<RB, WB, NBUF, tile_f64::Interp>(amps, P);
+}
+
+template <int RB, int WB, int NBUF>
+__global__ void __launch_bounds__(32 << WB, 1)
+k_tile_pass_f32(float2* __restrict__ amps, const __grid_constant__ TileParams P) {
+    tile_f32::tile_pass_body<RB, WB, NBUF, tile_f32::Interp>(amps, P);
 }
 
 } // namespace
 
-void launch_tile_pass(double2* amps, const TileParams& p, cudaStream_t s) {
+namespace {
+
+template <class T>
+void launch_interp(void (*kern)(T*, TileParams), void* amps, const TileParams& p, cudaStream_t s, size_t smem,
+                   bool& set) {
+    if (!set) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+        set = true;
+    }
+    uint64_t blocks = p.num_tiles;
+    if (blocks > 148) blocks = 148; // persistent: one CTA per SM
+    kern<<<static_cast<unsigned>(blocks), kTileThreads, smem, s>>>(static_cast<T*>(amps), p);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        cudaFuncAttributes fa{};
+        cudaFuncGetAttributes(&fa, kern);
+        char msg[256];
+        snprintf(msg, sizeof msg, "tile pass launch: %s (regs %d, max threads %d, static smem %zu, dyn smem %zu)",
+                 cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, smem);
+        throw DeviceError(msg);
+    }
+}
+
+} // namespace
+
+void launch_tile_pass(void* amps, const TileParams& p, cudaStream_t s) {
     if (launch_tile_pass_jit(amps, p, s)) { // straight-line kernel for this pass shape
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) throw DeviceError(std::string("jit tile pass launch: ") + cudaGetErrorString(e));
@@ -30,26 +61,14 @@ void launch_tile_pass(double2* amps, const TileParams& p, cudaStream_t s) {
         return;
     }
     constexpr int NBUF = 3;
-    auto kern = k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF>;
-    constexpr size_t smem = NBUF * (sizeof(double2) << kTileQubits);
-    static bool set = false;
-    if (!set) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-        set = true;
-    }
-    uint64_t blocks = p.num_tiles;
-    if (blocks > 148) blocks = 148; // persistent: one CTA per SM
-    kern<<<static_cast<unsigned>(blocks), kTileThreads, smem, s>>>(amps, p);
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) {
-        cudaFuncAttributes fa{};
-        cudaFuncGetAttributes(&fa, kern);
-        char msg[256];
-        snprintf(msg, sizeof msg,
-                 "tile pass launch: %s (regs %d, max threads %d, static smem %zu, dyn smem %zu)",
-                 cudaGetErrorString(e), fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes,
-                 smem);
-        throw DeviceError(msg);
+    if (p.single) {
+        static bool set = false;
+        launch_interp(k_tile_pass_f32<kPhaseRegBits, kTileWarpBits, NBUF>, amps, p, s,
+                      NBUF * (sizeof(float2) << kTileQubits), set);
+    } else {
+        static bool set = false;
+        launch_interp(k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF>, amps, p, s,
+                      NBUF * (sizeof(double2) << kTileQubits), set);
     }
     count_launch();
 }

@@ -161,8 +161,10 @@ _SIGS = {
     "qgpuPlanChunks": (_I, [_ULL, _ULL, ctypes.POINTER(ctypes.c_ulonglong)]),
     "qgpuModeledBytesPerRank": (_I, [_I, _I, _I, _I, _ULL, ctypes.POINTER(ctypes.c_ulonglong)]),
     "qgpuMaxQubits": (_I, [_ULL, _ULL, _I, _I, _I]),
-    "qgpuDeviceBytesPerRank": (_ULL, [_I, _I, _ULL]),
-    "qgpuDeviceMaxQubits": (_I, [_ULL, _I, _ULL, _I]),
+    "qgpuDeviceBytesPerRank": (_ULL, [_I, _I, _ULL, _I]),
+    "qgpuDeviceMaxQubits": (_I, [_ULL, _I, _ULL, _I, _I]),
+    "qgpuCreateQuregPrecision": (Qureg, [_I, QuESTEnv, _I, _I]),
+    "qgpuGetPrecision": (_I, [Qureg]),
     "qgpuSetJit": (None, [_I]),
     "qgpuGetJit": (_I, []),
     "qgpuJitWait": (None, []),
@@ -310,9 +312,20 @@ class Env:
 class QuregHandle:
     """Owns a Qureg; thin methods with QuEST names and a numpy state view."""
 
-    def __init__(self, env: Env, num_qubits: int, density: bool = False):
+    def __init__(self, env: Env, num_qubits: int, density: bool = False, precision: str = "double"):
+        """precision "double" (createQureg / createDensityQureg) or "single"
+        (Register(..., Precision::Single), register.hpp:53-54)."""
         self.env = env
-        self.h = call("createDensityQureg" if density else "createQureg", num_qubits, env.h)
+        if precision == "double":
+            self.h = call("createDensityQureg" if density else "createQureg", num_qubits, env.h)
+        elif precision == "single":
+            self.h = call("qgpuCreateQuregPrecision", num_qubits, env.h, int(density), 1)
+        else:
+            raise DomainError(f"precision must be 'single' or 'double', got {precision!r}")
+
+    @property
+    def precision(self) -> str:
+        return "single" if call("qgpuGetPrecision", self.h) == 1 else "double"
 
     @property
     def num_qubits(self) -> int:
@@ -413,15 +426,16 @@ def max_qubits(node_bytes: int, k: int, strategy: str = "full_clone", single: bo
     return r
 
 
-def device_bytes_per_rank(flat: int, k: int, chunk_amps: int = 1 << 24) -> int:
-    r = lib().qgpuDeviceBytesPerRank(flat, k, chunk_amps)
+def device_bytes_per_rank(flat: int, k: int, chunk_amps: int = 1 << 24, single: bool = False) -> int:
+    r = lib().qgpuDeviceBytesPerRank(flat, k, chunk_amps, int(single))
     if r == 0:
         check()
     return r
 
 
-def device_max_qubits(device_bytes: int, k: int, chunk_amps: int = 1 << 24, density: bool = False) -> int:
-    r = lib().qgpuDeviceMaxQubits(device_bytes, k, chunk_amps, int(density))
+def device_max_qubits(device_bytes: int, k: int, chunk_amps: int = 1 << 24, density: bool = False,
+                      single: bool = False) -> int:
+    r = lib().qgpuDeviceMaxQubits(device_bytes, k, chunk_amps, int(density), int(single))
     if r < 0:
         check()
     return r

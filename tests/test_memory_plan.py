@@ -84,3 +84,13 @@ def test_reference_named_mirror():
     m = qsim.MemoryModel(node_bytes=64 * GiB)
     assert [qsim.max_qubits(m, k) for k in range(4)] == [30, 31, 32, 33]
     assert qsim.modeled_bytes_per_rank(30, 0, "half_exchange", "single") == 12 * GiB
+
+
+def test_device_plan_single_precision():
+    """Single-precision registers: 8 B amplitudes and exchange sub-chunks (the
+    reduction scratch stays double-double), so one more qubit fits."""
+    hbm = 180 * 10**9
+    assert quest.device_max_qubits(hbm, 0, single=True) == 34
+    assert quest.device_max_qubits(hbm, 3, single=True) == 37
+    per = quest.device_bytes_per_rank(36, 3, single=True)
+    assert per == 64 * GiB + 2 * (1 << 24) * 8 + (592 + 8 + 1) * 16
