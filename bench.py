@@ -42,7 +42,20 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 METRIC = "effective HBM GB/s (gates x 2x16x2^n B / time), layered random circuit, 30 qubits per GPU"
+# --precision single: 8-byte amplitudes, the same
+# per-gate accounting with 8 B
+METRIC_SINGLE = ("effective HBM GB/s (gates x 2x8x2^n B / time), layered random circuit, "
+                 "30 qubits per GPU, single precision")
 UNIT = "GB/s"
+AMP = 16  # bytes per amplitude (set from --precision)
+
+
+def metric_name():
+    return METRIC_SINGLE if AMP == 8 else METRIC
+
+
+def dtype_name():
+    return "c64 (f32 pairs)" if AMP == 8 else "c128 (f64 pairs)"
 
 
 def parse_args():
@@ -58,6 +71,8 @@ def parse_args():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--fusion", type=int, default=0, help="0 fused, 1 pass per op, 2 simple kernels")
     p.add_argument("--reg-qubits", type=int, default=0)
+    p.add_argument("--precision", choices=["double", "single"], default="double",
+                   help="register precision (the headline is double)")
     p.add_argument("--jit", type=int, default=None,
                    help="per-pass JIT: 0 off, 1 on (default; env QGPU_JIT=off|sync also applies)")
     return p.parse_args()
@@ -128,7 +143,7 @@ def circuit_for(n: int, depth: int, seed: int):
 
 
 def effective_bytes(n: int, gates: int) -> float:
-    return gates * 2.0 * 16.0 * (2.0 ** n)
+    return gates * 2.0 * AMP * (2.0 ** n)
 
 
 # ------------------------------------------------------------ CPU reference
@@ -141,22 +156,22 @@ def cpu_reference(n: int, circuit, gates: int, reps: int, workers: int, seed: in
 
     sub = type(circuit)(circuit.num_qubits, circuit.depth, circuit.ops[:gates])
     ops = to_oracle_ops(sub)
+    single = AMP == 8
     if oracle.ref_available():
-        secs = oracle.ref_time_ops(n, ops, workers, reps)
+        secs = oracle.ref_time_ops(n, ops, workers, reps, single=single)
         kind = "reference"
     else:  # restatement (single-threaded C)
-        import numpy as np
-
-        amps = oracle.zero_state(n)
+        amps = oracle.zero_state_f(n) if single else oracle.zero_state(n)
+        run = oracle.restated().orc_run_ops_f if single else oracle.restated().orc_run_ops
         secs = []
         for _ in range(reps):
             t0 = time.perf_counter()
-            oracle.restated().orc_run_ops(n, 0, len(ops), ops.ctypes.data, amps.ctypes.data)
+            run(n, 0, len(ops), ops.ctypes.data, amps.ctypes.data)
             secs.append(time.perf_counter() - t0)
         kind, workers = "port", 1
     vals = [effective_bytes(n, gates) / s / 1e9 for s in secs]
     sample = (f"first {gates} gates of the {n}-qubit depth-{circuit.depth} layered circuit "
-              f"(seed {seed}), qsim::Register + apply_controlled_gate, "
+              f"(seed {seed}), qsim::Register({'Single' if single else 'Double'}) + apply_controlled_gate, "
               f"workers={workers}, allocation/init excluded")
     return vals, kind, workers, sample
 
@@ -174,13 +189,14 @@ def run_reference_arm(args):
     v = statistics.median(timed)
     ms_gate = effective_bytes(n, 1) / (v * 1e9) * 1e3
     line = {
-        "impl": "reference", "metric": METRIC, "value": round(v, 3), "unit": UNIT,
+        "impl": "reference", "metric": metric_name(), "value": round(v, 3), "unit": UNIT,
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(ms_gate * args.cpu_gates, 3), "ms_per_gate": round(ms_gate, 3),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "c128 (f64 pairs)",
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": dtype_name(),
         "data": "synthetic seeded circuit",
         "config": {"workload": f"layered random circuit, {n} qubits, depth {args.depth}, seed {args.seed}",
-                   "qubits": n, "sample_gates": args.cpu_gates, "l2": "state 16 GiB >> L2"},
+                   "qubits": n, "sample_gates": args.cpu_gates, "precision": args.precision,
+                   "l2": f"state {AMP << n >> 30} GiB >> L2"},
         "cpu_baseline": {"value": round(v, 3), "unit": UNIT, "cores": workers, "kind": kind, "sample": sample},
         "e2e": {"value": round(v, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
@@ -221,7 +237,7 @@ def run_ours(args):
     n = args.local_qubits + k
     circuit = circuit_for(n, args.depth, args.seed)
     gates = len(circuit.ops)
-    q = quest.QuregHandle(env, n)
+    q = quest.QuregHandle(env, n, precision=args.precision)
     stream = torch.cuda.ExternalStream(env.stream)
 
     def barrier():
@@ -252,7 +268,10 @@ def run_ours(args):
         start.record(stream)
         for _ in range(args.steps):
             C.apply_circuit(q, circuit)
-        q.flush()
+            # a step ends its last pass (an async launch, no sync), so every
+            # step runs the pass shapes the warm-up compiled; without it the
+            # pass boundaries drift across step junctions
+            q.flush()
         stop.record(stream)
         barrier()
     ms_launch, kinds = env.profile_stop()
@@ -271,14 +290,14 @@ def run_ours(args):
     traffic = None
     try:
         t = json.loads((ROOT / "profiles" / "traffic.json").read_text())["k_tile_pass"]
-        if t["local_qubits"] == args.local_qubits:
+        if t["local_qubits"] == args.local_qubits and t.get("amp_bytes", 16) == AMP:
             traffic = t["bytes"]
     except Exception:
         pass
     pass_ms = ms_launch[kinds == 0]
     exch_ms = ms_launch[kinds == 2]  # per-gate exchanges (swaps off)
     swap_ms = ms_launch[kinds == 5]  # global<->local qubit swaps
-    per_launch_bytes = 2.0 * 16.0 * (2.0 ** args.local_qubits)
+    per_launch_bytes = 2.0 * AMP * (2.0 ** args.local_qubits)
     achieved = per_launch_bytes / (float(pass_ms.mean()) / 1e3) / 1e9 if pass_ms.size else None
     share = float(pass_ms.sum()) / float(ms_launch.sum()) if ms_launch.size else None
 
@@ -306,7 +325,7 @@ def run_ours(args):
         env.set_fusion(0, 0, 0)
         p1 = ms1[k1 == 0]
         if p1.size:
-            gbs = 2.0 * 16.0 * (2.0 ** args.local_qubits) / (float(p1.mean()) / 1e3) / 1e9
+            gbs = 2.0 * AMP * (2.0 ** args.local_qubits) / (float(p1.mean()) / 1e3) / 1e9
             single = {"gates": int(p1.size), "avg_pass_ms": round(float(p1.mean()), 4),
                       "achieved_GBps": round(gbs, 1), "frac": round(gbs / peaks()[0]["hbm_gbs"], 4),
                       "what": "one gate per tile pass (fusion mode 1), same kernel, same bytes per pass"}
@@ -331,8 +350,8 @@ def run_ours(args):
     e2e = effective_bytes(n, gates) / e2e_t / 1e9
     # host->device bytes per step: each fused pass carries its op list as
     # kernel parameters (sizeof(PassParams) = 4528 B + the state pointer), and
-    # initZeroState writes amplitude 0 (16 B).
-    h2d = int(passes / args.steps * 4536) + 16
+    # initZeroState writes amplitude 0 (16 B, or 8 B single).
+    h2d = int(passes / args.steps * 4536) + AMP
     d2h = 16 * max(1, world)
 
     cpu = None
@@ -346,14 +365,15 @@ def run_ours(args):
 
     if rank == 0:
         line = {
-            "metric": METRIC, "value": round(value, 1), "unit": UNIT, "n_gpus": world,
+            "metric": metric_name(), "value": round(value, 1), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(elapsed / args.steps, 3),
             "ms_per_gate": round(ms_gate, 4), "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "c128 (f64 pairs)", "data": "synthetic seeded circuit",
+            "vs_baseline": None, "dtype": dtype_name(), "data": "synthetic seeded circuit",
             "config": {"workload": f"layered random circuit, {n} qubits, depth {args.depth}, seed {args.seed}",
                        "qubits": n, "local_qubits": args.local_qubits, "gates": gates,
                        "parallelism": f"amplitude partition over {world} GPU(s)",
-                       "l2": "state 16 GiB per GPU >> 126 MB L2 (no flush needed)",
+                       "precision": args.precision,
+                       "l2": f"state {AMP << args.local_qubits >> 30} GiB per GPU >> 126 MB L2 (no flush needed)",
                        "passes_per_step": passes / args.steps, "fusion": args.fusion,
                        "jit": {"mode": quest.lib().qgpuGetJit(), "kernels": quest.jit_stats()[0],
                                "failed": quest.jit_stats()[1],
@@ -377,7 +397,7 @@ def run_ours(args):
         if exch_ms.size or swap_ms.size:
             # bytes each way per rank: a whole partition per exchange gate,
             # half a partition per qubit swap
-            part = 16.0 * (2.0 ** args.local_qubits)
+            part = AMP * (2.0 ** args.local_qubits)
             moved = part * exch_ms.size + 0.5 * part * swap_ms.size
             t_s = (float(exch_ms.sum()) + float(swap_ms.sum())) / 1e3
             nv = moved / t_s / 1e9
@@ -394,7 +414,9 @@ def run_ours(args):
 
 
 def main():
+    global AMP
     args = parse_args()
+    AMP = 8 if args.precision == "single" else 16
     if args.impl == "reference":
         run_reference_arm(args)
     else:

@@ -101,6 +101,7 @@ def ref():
         L.ref_partition_info.argtypes = [ctypes.c_int] * 4 + [ctypes.POINTER(ctypes.c_int)] * 2
         L.ref_enumerate_pairs.argtypes = [ctypes.c_int, ctypes.c_int, _vp]
         L.ref_time_ops.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _dp]
+        L.ref_time_ops_prec.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _dp]
     return _ref_lib
 
 
@@ -226,10 +227,11 @@ def ref_reductions(nq: int, amps: np.ndarray, density: bool = False):
     return norm.value, complex(tr.value, ti.value), pur.value
 
 
-def ref_time_ops(nq: int, ops, workers: int, reps: int, density: bool = False) -> list[float]:
+def ref_time_ops(nq: int, ops, workers: int, reps: int, density: bool = False,
+                 single: bool = False) -> list[float]:
     ops = as_ops(ops)
     secs = (ctypes.c_double * reps)()
-    _check(ref().ref_time_ops(nq, int(density), len(ops), _ptr(ops), workers, reps, secs))
+    _check(ref().ref_time_ops_prec(nq, int(density), int(single), len(ops), _ptr(ops), workers, reps, secs))
     return list(secs)
 
 

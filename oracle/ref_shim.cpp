@@ -342,10 +342,11 @@ int ref_enumerate_pairs(int n, int target, unsigned long long* out_lo_hi) {
 
 // CPU baseline timer: allocation + init are outside the clock (PAPER.md:339,
 // SPEC.md:499-507); returns seconds of the op loop for each of `reps` reps.
-int ref_time_ops(int num_qubits, int density, int nops, const orc_op* ops,
-                 int workers, int reps, double* seconds) {
+int ref_time_ops_prec(int num_qubits, int density, int single, int nops, const orc_op* ops,
+                      int workers, int reps, double* seconds) {
     return guarded([&] {
-        qsim::Register reg(num_qubits, kind_of(density));
+        qsim::Register reg(num_qubits, kind_of(density),
+                           single ? qsim::Precision::Single : qsim::Precision::Double);
         for (int r = 0; r < reps; ++r) {
             reg.init_zero_state();
             const auto t0 = std::chrono::steady_clock::now();
@@ -355,6 +356,11 @@ int ref_time_ops(int num_qubits, int density, int nops, const orc_op* ops,
             seconds[r] = std::chrono::duration<double>(t1 - t0).count();
         }
     });
+}
+
+int ref_time_ops(int num_qubits, int density, int nops, const orc_op* ops,
+                 int workers, int reps, double* seconds) {
+    return ref_time_ops_prec(num_qubits, density, 0, nops, ops, workers, reps, seconds);
 }
 
 } // extern "C"

@@ -48,7 +48,7 @@ def _env(ranks_log2: int, strategy: str) -> quest.Env:
 
 def _modeled(flat: int, k: int, strategy: str, precision: str, chunk: int) -> int:
     if strategy == "swap":
-        return quest.device_bytes_per_rank(flat, k, chunk)
+        return quest.device_bytes_per_rank(flat, k, chunk, precision == "single")
     block = min(chunk, 1 << (flat - k)) if strategy == "per_amplitude" else 1
     return quest.modeled_bytes_per_rank(flat, k, strategy, precision == "single", block)
 
@@ -82,14 +82,12 @@ def bench_random_circuit(n: int, depth: int, seed: int, ranks_log2: int = 0, str
                          reps: int = 5, warmup: int = 3, kind: str = "statevector",
                          precision: str = "double", circuit: C.Circuit | None = None) -> list[dict]:
     """one BenchRecord per timed repetition."""
-    if precision != "double":
-        raise quest.DomainError("this runtime computes in double precision only")
     density = kind == "density"
     c = circuit if circuit is not None else C.reference_random_circuit(n, depth, seed)
     env = _env(ranks_log2, strategy)
     ranks = 1 << ranks_log2
     try:
-        q = quest.QuregHandle(env, n, density)
+        q = quest.QuregHandle(env, n, density, precision=precision)
         try:
             gates = max(1, len(c.ops))
             flat = 2 * n if density else n
@@ -117,7 +115,8 @@ def bench_random_circuit(n: int, depth: int, seed: int, ranks_log2: int = 0, str
 
 
 def bench_rotation_sweep(n: int, ranks_log2: int = 0, axis=(1.0, 0.0, 0.0), angle: float = 0.3,
-                         targets=None, strategy: str = "per_amplitude", reps: int = 5) -> list[dict]:
+                         targets=None, strategy: str = "per_amplitude", reps: int = 5,
+                         precision: str = "double") -> list[dict]:
     """one record per target (median of `reps` timings of a
     single rotation), flagged communicated when the target is a rank bit."""
     targets = list(range(n)) if targets is None else list(targets)
@@ -125,9 +124,9 @@ def bench_rotation_sweep(n: int, ranks_log2: int = 0, axis=(1.0, 0.0, 0.0), angl
     ranks = 1 << ranks_log2
     local = n - ranks_log2
     try:
-        q = quest.QuregHandle(env, n)
+        q = quest.QuregHandle(env, n, precision=precision)
         try:
-            modeled = _modeled(n, ranks_log2, strategy, "double", 1 << 24)
+            modeled = _modeled(n, ranks_log2, strategy, precision, 1 << 24)
             out = []
             for t in targets:
                 # apply_single_qubit_rotation (kernels.cpp:124-132): R_n(angle)
@@ -216,7 +215,8 @@ def main(argv=None) -> int:
         elif a.mode == "sweep":
             tg = [int(x) for x in a.targets.split(",")] if a.targets else None
             strategy = "per_amplitude" if a.strategy == "swap" and a.ranks_log2 == 0 else a.strategy
-            rows = bench_rotation_sweep(a.qubits, a.ranks_log2, targets=tg, strategy=strategy, reps=a.reps)
+            rows = bench_rotation_sweep(a.qubits, a.ranks_log2, targets=tg, strategy=strategy, reps=a.reps,
+                                        precision=a.precision)
             emit(rows, SWEEP_FIELDS, a.format, out)
             r = slowdown_ratio(rows)
             if r is not None:

@@ -243,7 +243,7 @@ int QuregImpl::max_phases() const {
 
 bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
     if (phases.empty()) phases.push_back(PhaseState{});
-    if (pair && op.q0 >= kFixedLaneBits) {
+    if (pair && op.q0 >= lane_fixed()) {
         const int q = op.q0;
         PhaseState& ph = phases.back();
         const bool in_phase = std::find(ph.regs.begin(), ph.regs.end(), q) != ph.regs.end();
@@ -349,8 +349,8 @@ void QuregImpl::enqueue_phys(const FlatOp& op) {
     if (op.kind == FK_DEPOL) {
         // fused into the tile pass when both qubits can be register qubits
         // of a phase (not lane-only qubits 0-2); else its own pass
-        const bool fusable = use_tile() && env->fusion_mode == 0 && op.q0 >= kFixedLaneBits &&
-                             op.q1 >= kFixedLaneBits && op.q0 < local_qubits && op.q1 < local_qubits;
+        const bool fusable = use_tile() && env->fusion_mode == 0 && op.q0 >= lane_fixed() &&
+                             op.q1 >= lane_fixed() && op.q0 < local_qubits && op.q1 < local_qubits;
         if (!fusable) {
             flush_pass();
             run_depol(op);
@@ -499,9 +499,13 @@ void QuregImpl::launch_tile() {
         // lane bits 3-4: in the last phase tile bits 3, 4 unless registers
         // (tile bits 0-4 are never warp bits there: per-warp segments);
         // earlier phases prefer bits of `pref`
+        // single precision: tile bit 3 is always lane bit 3 (8-byte
+        // amplitudes: lanes must span 16 consecutive amplitudes to cover the
+        // 32 shared-memory banks; place_tile never makes qubit 3 a register)
+        if (single) LB[p].push_back(3);
         if (last) {
             for (int t = kFixedLaneBits; t < kTileQubits && LB[p].size() < 2; ++t)
-                if (!has(RB[p], t)) LB[p].push_back(t);
+                if (!has(RB[p], t) && !has(LB[p], t)) LB[p].push_back(t);
         } else {
             // qubits 3, 4 targeted by this phase's pair ops (as lane ops,
             // place_tile) must stay lane bits
