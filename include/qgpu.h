@@ -141,6 +141,11 @@ int qgpuPlanChunks(unsigned long long localLen, unsigned long long chunkAmps,
 void qgpuSetJit(int mode);
 int qgpuGetJit(void);
 void qgpuJitWait(void);
+/* Stop the compile threads: queued shapes are dropped (they stay
+ * interpreted), in-flight compiles finish, the JIT is off for the rest of
+ * the process. Call before exit when compiles may be pending (the library
+ * also does it from an atexit handler; the Python wrapper from its own). */
+void qgpuJitShutdown(void);
 void qgpuJitStats(unsigned long long* kernels, unsigned long long* failed, unsigned long long* pending);
 /* Host-only (no GPU): compile a sample pass program for sm_100a with NVRTC.
  * Returns the cubin size, or -1 (message in log); *seconds = compile time. */

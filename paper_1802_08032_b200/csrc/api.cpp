@@ -1126,6 +1126,10 @@ void qgpuJitWait(void) {
     guarded_void("qgpuJitWait", [&] { qgpu::jit_wait(); });
 }
 
+void qgpuJitShutdown(void) {
+    guarded_void("qgpuJitShutdown", [&] { qgpu::jit_shutdown(); });
+}
+
 void qgpuJitStats(unsigned long long* kernels, unsigned long long* failed, unsigned long long* pending) {
     qgpu::jit_stats(kernels, failed, pending);
 }

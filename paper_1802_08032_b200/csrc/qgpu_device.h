@@ -116,6 +116,10 @@ constexpr int kTileGroupBits = QGPU_TILE_GROUP_BITS; // independent tile groups 
 constexpr int kTileQubits = kLaneQubits + kPhaseRegBits + kTileWarpBits;
 constexpr int kTileHigh = kTileQubits - kLaneQubits;
 constexpr int kTileThreads = 32 << (kTileWarpBits + kTileGroupBits); // 512 (16 warps)
+// Resident tile-pass CTAs per SM: single precision holds its 8 register
+// amplitudes in 16 registers, so two CTAs (64 registers per thread, 2 x 96 KiB
+// of stages) fit and double the warps that hide shared-memory latency.
+constexpr int kTileCtasF64 = 1, kTileCtasF32 = 2;
 constexpr int kMaxPhases = 8;
 constexpr int kMaxTileOps = 63; // + the stop bit of a phase fits a 64-bit op mask
 

@@ -34,6 +34,7 @@ bool launch_tile_pass_jit(void* amps, const TileParams& params, cudaStream_t s);
 void jit_wait();              // block until every queued compile finished
 void jit_set_mode(int mode);  // 0 off, 1 background compiles, 2 compile before first use
 int jit_mode();
+void jit_shutdown();
 void jit_stats(unsigned long long* kernels, unsigned long long* failed, unsigned long long* pending);
 int jit_selftest(char* log, int len, double* seconds); // host only: cubin bytes or -1
 

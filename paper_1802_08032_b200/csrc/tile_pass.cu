@@ -21,7 +21,7 @@ k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
 }
 
 template <int RB, int WB, int NBUF>
-__global__ void __launch_bounds__(32 << WB, 1)
+__global__ void __launch_bounds__(32 << WB, kTileCtasF32)
 k_tile_pass_f32(float2* __restrict__ amps, const __grid_constant__ TileParams P) {
     tile_f32::tile_pass_body<RB, WB, NBUF, tile_f32::Interp>(amps, P);
 }
@@ -32,13 +32,13 @@ namespace {
 
 template <class T>
 void launch_interp(void (*kern)(T*, TileParams), void* amps, const TileParams& p, cudaStream_t s, size_t smem,
-                   bool& set) {
+                   bool& set, int ctas_per_sm) {
     if (!set) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
         set = true;
     }
     uint64_t blocks = p.num_tiles;
-    if (blocks > 148) blocks = 148; // persistent: one CTA per SM
+    if (blocks > 148u * ctas_per_sm) blocks = 148u * ctas_per_sm; // persistent
     kern<<<static_cast<unsigned>(blocks), kTileThreads, smem, s>>>(static_cast<T*>(amps), p);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) {
@@ -64,11 +64,11 @@ void launch_tile_pass(void* amps, const TileParams& p, cudaStream_t s) {
     if (p.single) {
         static bool set = false;
         launch_interp(k_tile_pass_f32<kPhaseRegBits, kTileWarpBits, NBUF>, amps, p, s,
-                      NBUF * (sizeof(float2) << kTileQubits), set);
+                      NBUF * (sizeof(float2) << kTileQubits), set, kTileCtasF32);
     } else {
         static bool set = false;
         launch_interp(k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF>, amps, p, s,
-                      NBUF * (sizeof(double2) << kTileQubits), set);
+                      NBUF * (sizeof(double2) << kTileQubits), set, kTileCtasF64);
     }
     count_launch();
 }

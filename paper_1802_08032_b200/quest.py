@@ -9,6 +9,7 @@ raises the Python twin of the reference's exception class (types.hpp:31-55).
 """
 from __future__ import annotations
 
+import atexit
 import ctypes
 import os
 from pathlib import Path
@@ -168,6 +169,7 @@ _SIGS = {
     "qgpuSetJit": (None, [_I]),
     "qgpuGetJit": (_I, []),
     "qgpuJitWait": (None, []),
+    "qgpuJitShutdown": (None, []),
     "qgpuJitStats": (None, [_VP, _VP, _VP]),
     "qgpuJitSelfTest": (_I, [ctypes.c_char_p, _I, ctypes.POINTER(ctypes.c_double)]),
     "qgpuProfileStart": (None, [QuESTEnv]),
@@ -192,6 +194,9 @@ def lib():
             fn.restype = res
             fn.argtypes = args
         _lib = L
+        # compiles still queued at interpreter exit are dropped and the compile
+        # threads joined before any library tears down (qgpuJitShutdown)
+        atexit.register(L.qgpuJitShutdown)
     return _lib
 
 

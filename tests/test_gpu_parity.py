@@ -456,23 +456,33 @@ def test_jit_equals_interpreter_multi_phase(monkeypatch, n, phases):
         e.destroy()
 
 
-def test_exit_with_jit_compiles_pending(tmp_path):
-    """A process that exits while the JIT still has compiles queued shuts the
-    compile threads down cleanly (regression: a function-local static was
-    destroyed before the engine joined its threads, corrupting the heap)."""
+@pytest.mark.parametrize("delay", [0.0, 0.02, 0.08])
+@pytest.mark.parametrize("python_atexit", [True, False])
+def test_exit_with_jit_compiles_pending(tmp_path, delay, python_atexit):
+    """A process that exits while the JIT still has compiles queued or in
+    flight shuts the compile threads down cleanly (regressions: a
+    function-local static destroyed before the engine joined its threads;
+    NVRTC's lazily built statics destroyed at exit under a running
+    nvrtcCompileProgram — a segfault). Covered with the Python wrapper's
+    atexit hook and with the library's own (hook removed)."""
     import subprocess
     import sys
     from pathlib import Path
 
     root = Path(__file__).resolve().parent.parent
     script = (
-        "import sys; sys.path.insert(0, %r)\n"
+        "import sys, time, atexit; sys.path.insert(0, %r)\n"
         "from paper_1802_08032_b200 import circuits as C, quest\n"
         "from tests.harness import random_gate_circuit\n"
         "env = quest.Env(); q = quest.QuregHandle(env, 18)\n"
+        "%s"
         "C.apply_circuit(q, random_gate_circuit(18, 400, 5, max_controls=2))\n"
-        "q.flush(); print('pending', quest.jit_stats()[2])\n" % str(root))
-    r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300,
-                       cwd=str(root), env={**__import__("os").environ, "QGPU_JIT_OPTS": "-DQGPU_X=1"})
-    assert r.returncode == 0, r.stderr[-2000:]
-    assert "corrupt" not in r.stderr and "free()" not in r.stderr, r.stderr[-2000:]
+        "q.flush(); print('pending', quest.jit_stats()[2])\n"
+        "t = time.time()\n"
+        "while time.time() - t < %r: pass\n"
+        % (str(root), "" if python_atexit else "atexit.unregister(quest.lib().qgpuJitShutdown)\n", delay))
+    for _ in range(3):
+        r = subprocess.run([sys.executable, "-c", script], capture_output=True, text=True, timeout=300,
+                           cwd=str(root), env={**__import__("os").environ, "QGPU_JIT_OPTS": "-DQGPU_X=1"})
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert "corrupt" not in r.stderr and "free()" not in r.stderr, r.stderr[-2000:]
