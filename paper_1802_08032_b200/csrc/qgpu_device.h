@@ -197,6 +197,10 @@ struct TilePhase {
 struct TileParams {
     uint64_t num_tiles;
     uint64_t global_offset;
+    // local qubits outside the tile that every op of the pass needs at 1
+    // (common outer controls, outer diagonal targets with a == 1): only the
+    // tiles with those bits set are visited; the others stay untouched in HBM
+    uint64_t skip_ones;
     int32_t num_phases;
     int32_t fin_run;                       // a warp's segments come in HBM runs of 2^fin_run
     int32_t high_pos[kTileHigh];           // global qubits of tile bits 5.. (any order)

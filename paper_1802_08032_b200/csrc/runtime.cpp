@@ -414,13 +414,14 @@ void QuregImpl::flush_pass() {
 // printed at exit (scheduler / kernel tuning aid; off by default).
 namespace {
 struct PassStats {
-    uint64_t passes = 0, phases = 0, ops = 0, outer = 0;
+    uint64_t passes = 0, phases = 0, ops = 0, outer = 0, skipping = 0;
     uint64_t code[64] = {};
     ~PassStats() {
         if (!passes) return;
-        std::fprintf(stderr, "[qgpu pass stats] passes %llu, phases/pass %.2f, ops/pass %.2f, outer-controlled %.1f%%\n",
+        std::fprintf(stderr, "[qgpu pass stats] passes %llu, phases/pass %.2f, ops/pass %.2f, outer-controlled %.1f%%, "
+                     "tile-skipping passes %llu\n",
                      (unsigned long long)passes, double(phases) / passes, double(ops) / passes,
-                     100.0 * double(outer) / double(ops ? ops : 1));
+                     100.0 * double(outer) / double(ops ? ops : 1), (unsigned long long)skipping);
         for (int c = 0; c < 64; ++c)
             if (code[c])
                 std::fprintf(stderr, "  code %2d: %6.2f per pass\n", c, double(code[c]) / passes);
@@ -437,6 +438,7 @@ bool pass_stats_enabled() {
 void record_pass_stats(const TileParams& P) {
     const int nops = P.phases[P.num_phases - 1].op_end;
     ++g_pass_stats.passes;
+    if (P.skip_ones) ++g_pass_stats.skipping;
     g_pass_stats.phases += P.num_phases;
     g_pass_stats.ops += nops;
     for (int k = 0; k < nops; ++k) {
@@ -450,8 +452,19 @@ void QuregImpl::launch_tile() {
     // lowest unused local qubits (qubits 5, 6, 7 let a warp's last-phase
     // segments merge into longer bulk copies, see P.fin_run).
     std::vector<int> high = tile_high;
-    for (int q = kLaneQubits; static_cast<int>(high.size()) < kTileHigh && q < local_qubits; ++q)
-        if (std::find(high.begin(), high.end(), q) == high.end()) high.push_back(q);
+    // qubits every op needs at 1 (common controls, diagonal targets with
+    // a == 1) are topped up last: outside the tile they let the pass skip
+    // every tile where they are 0 (TileParams.skip_ones)
+    uint64_t need = ~uint64_t{0};
+    for (const FlatOp& op : pending) {
+        uint64_t m = op.kind == FK_GATE ? op.cmask : 0;
+        if (op.kind == FK_GATE && op.cls == CLS_DIAG && (op.flags & DF_A_ONE)) m |= uint64_t{1} << op.q0;
+        need &= m;
+    }
+    for (int pass = 0; pass < 2; ++pass)
+        for (int q = kLaneQubits; static_cast<int>(high.size()) < kTileHigh && q < local_qubits; ++q)
+            if (std::find(high.begin(), high.end(), q) == high.end() && (pass == 1 || !((need >> q) & 1)))
+                high.push_back(q);
     std::sort(high.begin(), high.end());
     auto tbit = [&](int q) -> int { // tile bit of a local qubit, -1 if outside
         if (q >= 0 && q < kLaneQubits) return q;
@@ -788,10 +801,21 @@ void QuregImpl::launch_tile() {
             std::memcpy(to.m, op.m, sizeof(to.m));
         }
     }
+    // Bits every op needs at 1 outside the tile: local ones shrink the tile
+    // enumeration (the other tiles are left untouched in HBM: a lone
+    // controlled gate reads and writes half the state), rank ones skip the
+    // shard (the reference's rank-id control skip, distributed.cpp:143-145)
+    uint64_t common = ~uint64_t{0};
+    for (int k = 0; k < P.phases[P.num_phases - 1].op_end; ++k) common &= P.ops[k].outer_cmask;
+    const uint64_t local_mask = local_len - 1;
+    P.skip_ones = common & local_mask;
+    const uint64_t rank_need = common & ~local_mask;
+    P.num_tiles >>= __builtin_popcountll(P.skip_ones);
     if (pass_stats_enabled()) record_pass_stats(P);
     ProfScope prof(env, PK_PASS);
     for (auto& s : shards) {
         P.global_offset = goff(s);
+        if ((P.global_offset & rank_need) != rank_need) continue;
         launch_tile_pass(s.amps, P, env->stream);
     }
     cuda_check(cudaGetLastError(), "tile pass launch");

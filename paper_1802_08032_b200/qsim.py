@@ -124,13 +124,14 @@ class Register:
 
     def __init__(self, num_qubits: int, kind: str = STATE_VECTOR, precision: str = "double",
                  env: quest.Env | None = None):
-        if precision != "double":
-            raise DomainError("only double precision is built (SURVEY.md §8(f) item 4)")
+        if precision not in ("single", "double"):
+            raise DomainError(f"unknown precision {precision!r}")
         if kind not in (STATE_VECTOR, DENSITY_MATRIX):
             raise DomainError(f"unknown register kind {kind!r}")
         self.env = env or default_env()
-        self._q = quest.QuregHandle(self.env, num_qubits, kind == DENSITY_MATRIX)
+        self._q = quest.QuregHandle(self.env, num_qubits, kind == DENSITY_MATRIX, precision=precision)
         self._kind = kind
+        self._precision = precision
 
     # register.hpp accessors
     def num_qubits(self) -> int:
@@ -140,7 +141,7 @@ class Register:
         return self._kind
 
     def precision(self) -> str:
-        return "double"
+        return self._precision
 
     def flat_qubits(self) -> int:
         return self._q.flat_qubits
@@ -165,8 +166,11 @@ class Register:
         return quest.call("qgpuNormSquared", self._q.h)
 
     def amps(self) -> np.ndarray:
-        """Host copy of the whole flat vector (for tests and result export)."""
-        return self._q.state()
+        """Host copy of the whole flat vector (for tests and result export):
+        complex128, or complex64 for a single-precision register (the
+        reference's data32(), register.hpp:30)."""
+        a = self._q.state()
+        return a.astype(np.complex64) if self._precision == "single" else a
 
     def set_amps(self, amps: np.ndarray):
         self._q.set_state(amps)

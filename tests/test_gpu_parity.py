@@ -486,3 +486,58 @@ def test_exit_with_jit_compiles_pending(tmp_path, delay, python_atexit):
                            cwd=str(root), env={**__import__("os").environ, "QGPU_JIT_OPTS": "-DQGPU_X=1"})
         assert r.returncode == 0, r.stderr[-2000:]
         assert "corrupt" not in r.stderr and "free()" not in r.stderr, r.stderr[-2000:]
+
+
+def _common_control_circuit(n, seed, ctrl):
+    """Gates that all carry the controls `ctrl` (qubits outside most tiles),
+    interleaved with outer diagonal gates (a == 1: T, S, phase shifts)."""
+    rng = np.random.default_rng(seed)
+    names = ["H", "X", "Y", "RX", "RY", "RZ", "T", "S", "PHASE", "U", "Z"]
+    c = C.Circuit(n, 0, [])
+    free = [q for q in range(n) if q not in ctrl]
+    for _ in range(120):
+        nm = names[int(rng.integers(len(names)))]
+        t = int(free[int(rng.integers(len(free)))])
+        ang = float(rng.uniform(0, 6.3))
+        if nm == "U":
+            from tests.harness import random_unitary
+
+            c.ops.append(C.GateOp("U", t, controls=tuple(ctrl), matrix=tuple(random_unitary(rng))))
+        else:
+            c.ops.append(C.GateOp(nm, t, controls=tuple(ctrl), angle=ang))
+    return c
+
+
+@pytest.mark.parametrize("mode", [0, 1])
+@pytest.mark.parametrize("ctrl", [(15,), (14, 15), (13,)])
+def test_tile_skipping_common_outer_controls(env, mode, ctrl):
+    """Passes whose every op needs the same qubits outside the tile at 1 visit
+    only those tiles (TileParams.skip_ones); the rest of the state must come
+    through untouched. Fused passes and one op per pass, bit for bit."""
+    n = 16
+    env.set_fusion(mode, 48, 4)
+    try:
+        rng = np.random.default_rng(3)
+        init = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+        init /= np.linalg.norm(init)
+        c = _common_control_circuit(n, 11 + len(ctrl), ctrl)
+        c.ops += [C.GateOp("T", 15), C.GateOp("PHASE", 14, angle=0.4), C.GateOp("S", 13, controls=(15,))]
+        assert_parity(run_product(env, c, init=init), oracle_run(c, init=init))
+    finally:
+        env.set_fusion(0, 48, 4)
+
+
+@pytest.mark.parametrize("swaps", [False, True])
+def test_tile_skipping_rank_bit_controls(swaps):
+    """Controls on rank bits common to a whole pass skip the non-matching
+    ranks' launches (distributed.cpp:143-145 at pass level)."""
+    n, k = 15, 2
+    c = _common_control_circuit(n, 5, (14,))
+    c.ops += _common_control_circuit(n, 6, (13, 14)).ops
+    want = oracle_run(c)
+    e = quest.Env.loopback(1 << k)
+    e.set_qubit_swaps(swaps)
+    try:
+        assert_parity(run_product(e, c), want)
+    finally:
+        e.destroy()

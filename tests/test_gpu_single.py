@@ -206,3 +206,23 @@ def test_single_30q_forward_inverse_property(env):
         assert abs(abs(complex(a.real, a.imag)) - 1.0) < 1e-4
     finally:
         q.destroy()
+
+
+def test_single_qsim_mirror_register():
+    """qsim.Register(n, kind, "single") (register.hpp:53-54) through the
+    reference-named mirror: run_circuit then amps() as complex64, equal to the
+    reference's data32() bit for bit."""
+    from paper_1802_08032_b200 import qsim
+
+    c = C.layered_random_circuit(13, 4, 21)
+    r = qsim.Register(13, qsim.STATE_VECTOR, "single")
+    try:
+        assert r.precision() == "single"
+        qsim.run_circuit(c, r)
+        got = r.amps()
+        assert got.dtype == np.complex64
+        ops = to_oracle_ops(c)
+        want = oracle.ref_run_single(13, ops) if oracle.ref_available() else oracle.orc_run_f(13, ops)
+        assert np.array_equal(got, want)
+    finally:
+        r.destroy()
