@@ -67,6 +67,26 @@ int qgpuProfileStop(QuESTEnv env, double* ms, int* kinds, int maxRecords);
 Qureg qgpuCreateQuregPrecision(int numQubits, QuESTEnv env, int density, int precision);
 int qgpuGetPrecision(Qureg qureg); /* 1 or 2; -1 on error */
 
+/* ------------------------------------------------------------ run_circuit */
+/* One op of a circuit (96 bytes): kind 0 = a 2x2 gate `m` (re, im of m00,
+ * m01, m10, m11) on `target` with controls `ctrlMask` (bit c = qubit c), as
+ * apply_controlled_gate / apply_gate_to_density (kernels.cpp:105-112,
+ * density.cpp:85-116); kind 1 = apply_dephasing(target, prob); kind 2 =
+ * apply_depolarising(target, prob) (density.cpp:118-145). */
+typedef struct {
+    int kind;
+    int target;
+    unsigned long long ctrlMask;
+    double m[8];
+    double prob;
+    double reserved;
+} qgpuOp;
+/* run_circuit (circuit.cpp:239-247) in one call: all ops are validated first
+ * (an invalid one leaves the register untouched and reports which), then
+ * queued in order — the same results as one call per op, without a C-ABI
+ * crossing per gate. */
+void qgpuRunCircuit(Qureg qureg, const qgpuOp* ops, int numOps);
+
 /* --------------------------------------------------------- bulk state I/O */
 /* Interleaved (re, im) doubles of flat amplitudes [start, start + num). */
 void qgpuCopyStateToHost(Qureg qureg, long long int start, long long int num, double* out);

@@ -339,8 +339,35 @@ def apply_op(q, op: GateOp):
 
 
 def apply_circuit(q, circuit: Circuit):
+    """One QuEST C-ABI call per op (the per-gate entry points)."""
     for op in circuit.ops:
         apply_op(q, op)
+
+
+# qgpuOp (include/qgpu.h): 96-byte records, kind 0 gate / 1 dephase / 2 depolarise
+OP_DTYPE = [("kind", "<i4"), ("target", "<i4"), ("ctrl_mask", "<u8"), ("m", "<f8", (8,)),
+            ("prob", "<f8"), ("reserved", "<f8")]
+
+
+def op_array(circuit: Circuit):
+    """The circuit as a qgpuOp array for qgpuRunCircuit."""
+    import numpy as np
+
+    a = np.zeros(len(circuit.ops), dtype=np.dtype(OP_DTYPE, align=False))
+    for i, op in enumerate(circuit.ops):
+        if op.name == "DEPHASE":
+            a[i] = (1, op.target, 0, np.zeros(8), op.prob, 0.0)
+        elif op.name == "DEPOL":
+            a[i] = (2, op.target, 0, np.zeros(8), op.prob, 0.0)
+        else:
+            a[i] = (0, op.target, op.ctrl_mask(), np.array(op.m8()), 0.0, 0.0)
+    return a
+
+
+def run_circuit(q, circuit: Circuit):
+    """run_circuit (circuit.cpp:239-247) as one C-ABI call
+    (qgpuRunCircuit): all ops validated first, then queued."""
+    q.run_ops(op_array(circuit))
 
 
 def dagger(op: GateOp) -> GateOp:

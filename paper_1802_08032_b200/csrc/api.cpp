@@ -974,6 +974,90 @@ void mixDepolarising(Qureg qureg, int targetQubit, qreal prob) {
     });
 }
 
+// ------------------------------------------------------------ run_circuit
+
+// circuit.cpp:239-247 (run_circuit) as one call: every op is validated with
+// the rules of its single-op entry point before any is queued, so an invalid
+// op leaves the register untouched; then the ops are queued in order.
+void qgpuRunCircuit(Qureg qureg, const qgpuOp* ops, int numOps) {
+    guarded_void("qgpuRunCircuit", [&] {
+        QuregImpl* r = reg_of(qureg);
+        if (numOps < 0 || (numOps > 0 && !ops)) throw qgpu::DomainError("invalid op array");
+        std::vector<FlatOp> flat;
+        flat.reserve(static_cast<size_t>(numOps) * (r->density ? 2 : 1));
+        for (int i = 0; i < numOps; ++i) {
+            const qgpuOp& o = ops[i];
+            switch (o.kind) {
+            case 0: { // gate: apply_controlled_gate / apply_gate_to_density
+                check_qubit(r, o.target, "target");
+                if (o.ctrlMask >> r->N) {
+                    const int b = 63 - __builtin_clzll(o.ctrlMask);
+                    if (r->density)
+                        throw qgpu::DomainError("invalid qubit " + std::to_string(b) + " for " +
+                                                std::to_string(r->N) + "-qubit density matrix");
+                    throw qgpu::DomainError("invalid control qubit " + std::to_string(b));
+                }
+                if ((o.ctrlMask >> o.target) & 1)
+                    throw qgpu::DomainError("control qubit " + std::to_string(o.target) + " overlaps the target");
+                FlatOp op;
+                op.kind = FK_GATE;
+                op.q0 = o.target;
+                op.cmask = o.ctrlMask;
+                for (int k = 0; k < 8; ++k) {
+                    if (!std::isfinite(o.m[k])) throw qgpu::DomainError("matrix entries must be finite");
+                    op.m[k] = o.m[k];
+                }
+                op.cls = classify(op.m, &op.flags);
+                flat.push_back(op);
+                if (r->density) {
+                    FlatOp bra = op;
+                    bra.q0 = o.target + r->N;
+                    bra.cmask = o.ctrlMask << r->N;
+                    for (int k = 1; k < 8; k += 2) bra.m[k] = -op.m[k]; // GateMatrix::conjugate
+                    bra.cls = classify(bra.m, &bra.flags);
+                    flat.push_back(bra);
+                }
+                break;
+            }
+            case 1: { // apply_dephasing (density.cpp:118-130)
+                require_density(r, "dephasing");
+                check_qubit(r, o.target, "target");
+                if (!(o.prob >= 0.0 && o.prob <= 0.5))
+                    throw qgpu::DomainError("dephasing probability must lie in [0, 1/2], got " +
+                                            std::to_string(o.prob));
+                FlatOp op;
+                op.kind = FK_DEPHASE;
+                op.q0 = o.target;
+                op.q1 = o.target + r->N;
+                op.m[0] = 1.0 - 2.0 * o.prob;
+                flat.push_back(op);
+                break;
+            }
+            case 2: { // apply_depolarising (density.cpp:132-145)
+                require_density(r, "depolarising");
+                check_qubit(r, o.target, "target");
+                if (!(o.prob >= 0.0 && o.prob <= 0.75))
+                    throw qgpu::DomainError("depolarising probability must lie in [0, 3/4], got " +
+                                            std::to_string(o.prob));
+                FlatOp op;
+                op.kind = FK_DEPOL;
+                op.q0 = o.target;
+                op.q1 = o.target + r->N;
+                op.m[0] = 1.0 - 2.0 * o.prob / 3.0;
+                op.m[1] = 2.0 * o.prob / 3.0;
+                op.m[2] = 1.0 - 4.0 * o.prob / 3.0;
+                flat.push_back(op);
+                break;
+            }
+            default:
+                throw qgpu::DomainError("unknown op kind " + std::to_string(o.kind) + " at op " +
+                                        std::to_string(i));
+            }
+        }
+        for (const FlatOp& op : flat) r->enqueue(op);
+    });
+}
+
 // ------------------------------------------------------------- profiling
 
 void qgpuProfileStart(QuESTEnv env) {

@@ -286,10 +286,10 @@ def generate_random_circuit(num_qubits: int, depth: int, seed: int) -> C.Circuit
 
 
 def run_circuit(circuit: C.Circuit, reg: Register):
-    """circuit.cpp:239-247."""
+    """circuit.cpp:239-247, as one C-ABI call (qgpuRunCircuit)."""
     if reg.num_qubits() != circuit.num_qubits:
         raise DomainError(f"circuit is for {circuit.num_qubits} qubits but the register has {reg.num_qubits()}")
-    C.apply_circuit(reg.handle, circuit)
+    C.run_circuit(reg.handle, circuit)
 
 
 gate_counts = C.gate_counts

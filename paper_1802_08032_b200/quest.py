@@ -170,6 +170,7 @@ _SIGS = {
     "qgpuGetJit": (_I, []),
     "qgpuJitWait": (None, []),
     "qgpuJitShutdown": (None, []),
+    "qgpuRunCircuit": (None, [Qureg, _VP, _I]),
     "qgpuJitStats": (None, [_VP, _VP, _VP]),
     "qgpuJitSelfTest": (_I, [ctypes.c_char_p, _I, ctypes.POINTER(ctypes.c_double)]),
     "qgpuProfileStart": (None, [QuESTEnv]),
@@ -360,6 +361,13 @@ class QuregHandle:
     def set_state(self, amps: np.ndarray, start: int = 0):
         a = np.ascontiguousarray(amps, dtype=np.complex128)
         call("qgpuCopyStateFromHost", self.h, start, a.size, a.ctypes.data)
+
+    def run_ops(self, ops: np.ndarray):
+        """qgpuRunCircuit over a circuits.op_array() record array."""
+        a = np.ascontiguousarray(ops)
+        if a.dtype.itemsize != 96:
+            raise DomainError("op records must be 96-byte qgpuOp")
+        call("qgpuRunCircuit", self.h, a.ctypes.data, a.size)
 
     def apply_matrix(self, target: int, ctrl_mask: int, m8):
         m = np.ascontiguousarray(m8, dtype=np.float64)

@@ -541,3 +541,28 @@ def test_tile_skipping_rank_bit_controls(swaps):
         assert_parity(run_product(e, c), want)
     finally:
         e.destroy()
+
+
+@pytest.mark.parametrize("density", [False, True])
+def test_run_circuit_batch_equals_per_call(env, density):
+    """qgpuRunCircuit (run_circuit, circuit.cpp:239-247, one C-ABI call) gives
+    the per-call result and the oracle's, bit for bit; an invalid op anywhere
+    in the array leaves the register untouched."""
+    n = 6 if density else 14
+    c = random_gate_circuit(n, 150, seed=77, max_controls=2, channels=density)
+    q = quest.QuregHandle(env, n, density)
+    try:
+        C.run_circuit(q, c)
+        got = q.state()
+        assert_parity(got, oracle_run(c, density=density))
+        assert_parity(got, run_product(env, c, density=density))
+        bad = C.op_array(c)
+        bad[len(bad) // 2]["target"] = n  # out of range, mid-array
+        with pytest.raises(quest.DomainError, match="invalid"):
+            q.run_ops(bad)
+        chan = C.op_array(C.Circuit(n, 0, [C.GateOp("H", 0), C.GateOp("DEPOL", 1, prob=0.9)]))
+        with pytest.raises(quest.DomainError):
+            q.run_ops(chan)  # p > 3/4 (density) or a channel on a state vector
+        assert np.array_equal(q.state(), got)
+    finally:
+        q.destroy()

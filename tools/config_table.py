@@ -47,7 +47,7 @@ CONFIGS = {
 }
 
 
-def gpu_time(cfg, c):
+def gpu_time(cfg, c, batch=False):
     env = quest.Env()
     q = quest.QuregHandle(env, cfg["n"], cfg["density"])
     stream = torch.cuda.ExternalStream(env.stream)
@@ -56,7 +56,7 @@ def gpu_time(cfg, c):
     def step():
         if cfg is CONFIGS.get("C5"):
             q.initClassicalState(0x5A5A5A5A)
-        C.apply_circuit(q, c)
+        (C.run_circuit if batch else C.apply_circuit)(q, c)
         q.flush()
 
     try:
@@ -116,6 +116,9 @@ for name in a.only.split(","):
            "effective_TBps": round(B * len(c.ops) / (ms / 1e3) / 1e12, 2), "norm_after": norm}
     if extra:
         row.update(extra)
+    if name == "C1":  # host-bound: also through qgpuRunCircuit (one C-ABI call per step)
+        msb, _, _ = gpu_time(cfg, c, batch=True)
+        row.update({"ms_per_step_run_circuit": round(msb, 3), "ms_per_op_run_circuit": round(msb / len(c.ops), 4)})
     if not a.no_cpu and name in ("C1", "C2", "C4"):
         cms, workers = cpu_time(cfg, c)
         if cms is not None:
