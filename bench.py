@@ -73,6 +73,8 @@ def parse_args():
     p.add_argument("--reg-qubits", type=int, default=0)
     p.add_argument("--precision", choices=["double", "single"], default="double",
                    help="register precision (the headline is double)")
+    p.add_argument("--no-single", action="store_true",
+                   help="skip the single-precision side measurement of the double run")
     p.add_argument("--jit", type=int, default=None,
                    help="per-pass JIT: 0 off, 1 on (default; env QGPU_JIT=off|sync also applies)")
     return p.parse_args()
@@ -330,6 +332,37 @@ def run_ours(args):
                       "achieved_GBps": round(gbs, 1), "frac": round(gbs / peaks()[0]["hbm_gbs"], 4),
                       "what": "one gate per tile pass (fusion mode 1), same kernel, same bytes per pass"}
 
+    # side measurement: the same circuit on a single-precision register
+    # (Precision::Single, 2 x 8 B per amplitude per gate), device-timed the
+    # same way; not the headline
+    sp = None
+    if args.precision == "double" and not args.no_single and world == 1:
+        qs = quest.QuregHandle(env, n, precision="single")
+        for _ in range(max(2, args.warmup)):
+            C.apply_circuit(qs, circuit)
+            qs.flush()
+            env.sync()
+            quest.jit_wait()
+        barrier()
+        env.profile_start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            C.apply_circuit(qs, circuit)
+            qs.flush()
+        e1.record(stream)
+        barrier()
+        ms_s, k_s = env.profile_stop()
+        t_sp = e0.elapsed_time(e1)
+        p_s = ms_s[k_s == 0]
+        b_sp = 2.0 * 8 * 2.0 ** n
+        sp = {"metric": METRIC_SINGLE, "value": round(gates * args.steps * b_sp / (t_sp / 1e3) / 1e9, 1),
+              "unit": UNIT, "ms_per_gate": round(t_sp / (gates * args.steps), 4), "dtype": "c64 (f32 pairs)",
+              "roofline_frac": round(b_sp / (float(p_s.mean()) / 1e3) / 1e9 / pk["hbm_gbs"], 4) if p_s.size else None,
+              "avg_launch_ms": round(float(p_s.mean()), 4) if p_s.size else None,
+              "norm_error": abs(qs.calcTotalProb() - 1.0)}
+        qs.destroy()
+
     # e2e through the C-ABI from the host: init + gates + readback, wall clock
     e2e_vals = []
     for _ in range(max(1, min(args.steps, 3))):
@@ -392,6 +425,7 @@ def run_ours(args):
             "clocks": clocks.summary(),
             "check": {"norm_error_after_timed_steps": norm_error},
             "single_gate_pass": single,
+            "single_precision": sp,
             "cpu_baseline": cpu,
         }
         if exch_ms.size or swap_ms.size:
