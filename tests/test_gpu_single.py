@@ -226,3 +226,19 @@ def test_single_qsim_mirror_register():
         assert np.array_equal(got, want)
     finally:
         r.destroy()
+
+
+@pytest.mark.parametrize("n", [1, 2])
+@pytest.mark.parametrize("density", [False, True])
+def test_single_smallest_registers_and_empty_circuits(env, n, density):
+    """The smallest registers (1-2 qubits; a 1-qubit density matrix is a
+    2-qubit flat vector) in single precision, and empty op arrays (a no-op)."""
+    c = random_gate_circuit(n, 40, seed=9 + n, max_controls=1 if n > 1 else 0, channels=density)
+    q = quest.QuregHandle(env, n, density, precision="single")
+    try:
+        q.run_ops(C.op_array(C.Circuit(n, 0, [])))
+        C.run_circuit(q, c)
+        q.run_ops(C.op_array(C.Circuit(n, 0, [])))
+        assert_parity_f(q.state(), want_single(c, density))
+    finally:
+        q.destroy()
