@@ -566,3 +566,30 @@ def test_run_circuit_batch_equals_per_call(env, density):
         assert np.array_equal(q.state(), got)
     finally:
         q.destroy()
+
+
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_nccl_environment_single_rank(precision):
+    """The NCCL environment (qgpuCreateNcclEnv: communicator init, the NCCL
+    transport, all-gathered reductions) on one rank — the multi-GPU
+    plumbing runs on real hardware even with one GPU; results equal the
+    oracle's bit for bit."""
+    uid = quest.Env.nccl_unique_id()
+    e = quest.Env.nccl(0, 1, 0, uid)
+    try:
+        assert e.num_ranks == 1 and e.rank == 0
+        c = random_gate_circuit(14, 120, seed=123, max_controls=2)
+        q = quest.QuregHandle(e, 14, precision=precision)
+        C.run_circuit(q, c)
+        got = q.state()
+        ops = to_oracle_ops(c)
+        if precision == "single":
+            assert np.array_equal(got, oracle.orc_run_f(14, ops).astype(np.complex128))
+        else:
+            assert_parity(got, oracle_run(c))
+        w = got.astype(np.complex128)
+        assert abs(q.calcTotalProb() - float(np.sum(np.abs(w) ** 2))) < 1e-12
+        assert abs(q.calcProbOfOutcome(3, 1) - float(np.sum(np.abs(w[((np.arange(1 << 14) >> 3) & 1) == 1]) ** 2))) < 1e-12
+        q.destroy()
+    finally:
+        e.destroy()
