@@ -23,6 +23,15 @@ per GPU, gates on the top log2(N) qubits exchange over NCCL.
          /root/reference) on this host's cores, on the first G gates of the
          same circuit.
 
+  single_precision  side measurement (not the headline): the same circuit
+         on a Precision::Single register (2 x 8 B per amplitude per gate),
+         device-timed the same way (`--no-single` skips it; `--precision
+         single` makes it the measured arm).
+
+Each timed step is one whole circuit ending in a flush (an asynchronous
+launch of its last pass), so every step runs the pass shapes the warm-up
+compiled.
+
 --impl reference: the reference's own CPU implementation on the same
 config/metric, each step a bounded sample (first G gates).
 """

@@ -91,3 +91,16 @@ def test_jit_compiles_sample_pass_for_sm100a():
     host only, no GPU."""
     n, log, sec = quest.jit_selftest()
     assert n > 0, log
+
+
+def test_qgpu_op_records_match_the_checkers_layout():
+    """circuits.op_array (qgpuOp, include/qgpu.h) is byte-identical to the
+    oracle's 96-byte op records for gates, controls and both channels."""
+    import oracle
+    from paper_1802_08032_b200 import circuits as C
+    from tests.harness import random_gate_circuit, to_oracle_ops
+
+    c = random_gate_circuit(6, 80, seed=4, max_controls=3, channels=True)
+    a = C.op_array(c)
+    assert a.dtype.itemsize == 96 == oracle.OP_DTYPE.itemsize
+    assert a.tobytes() == to_oracle_ops(c).tobytes()
