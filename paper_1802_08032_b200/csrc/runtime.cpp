@@ -241,6 +241,16 @@ int QuregImpl::max_phases() const {
     return jit_mode() != 0 ? 3 : 2;
 }
 
+// single precision keeps tile bit 3 on lane bit 3 (QGPU_SP_PIN3=0 turns it
+// off: an A/B knob)
+bool QuregImpl::pin_lane3() const {
+    static const bool on = [] {
+        const char* e = std::getenv("QGPU_SP_PIN3");
+        return !(e && e[0] == '0');
+    }();
+    return single && on;
+}
+
 bool QuregImpl::place_tile(const FlatOp& op, bool pair) {
     if (phases.empty()) phases.push_back(PhaseState{});
     if (pair && op.q0 >= lane_fixed()) {
@@ -515,7 +525,7 @@ void QuregImpl::launch_tile() {
         // single precision: tile bit 3 is always lane bit 3 (8-byte
         // amplitudes: lanes must span 16 consecutive amplitudes to cover the
         // 32 shared-memory banks; place_tile never makes qubit 3 a register)
-        if (single) LB[p].push_back(3);
+        if (pin_lane3()) LB[p].push_back(3);
         if (last) {
             for (int t = kFixedLaneBits; t < kTileQubits && LB[p].size() < 2; ++t)
                 if (!has(RB[p], t) && !has(LB[p], t)) LB[p].push_back(t);

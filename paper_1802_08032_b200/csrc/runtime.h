@@ -132,7 +132,8 @@ struct QuregImpl {
     size_t amp_bytes() const { return single ? sizeof(float2) : sizeof(double2); }
     // qubits held by fixed lane bits in every tile phase: 0-2, and 3 in single
     // precision (runtime.cpp: launch_tile's shared-memory bank argument)
-    int lane_fixed() const { return single ? kFixedLaneBits + 1 : kFixedLaneBits; }
+    int lane_fixed() const { return pin_lane3() ? kFixedLaneBits + 1 : kFixedLaneBits; }
+    bool pin_lane3() const;
     // element `i` of a shard (or exchange buffer) as a byte address
     char* at(void* base, uint64_t i) const { return static_cast<char*>(base) + i * amp_bytes(); }
 
