@@ -88,6 +88,16 @@ def to_circuit(n, ops_):
     return c
 
 
+def single_workloads():
+    """name -> (num_qubits, density, circuit) for the single-precision vectors
+    (shared with tests/test_golden.py)."""
+    return {
+        "sp_layered_n13_d5_s3": (13, False, C.layered_random_circuit(13, 5, 3)),
+        "sp_random_n5_s99": (5, False, random_gate_circuit(5, 60, 99, max_controls=2)),
+        "sp_dm_noisy_n6_d3_s5": (6, True, C.layered_random_circuit(6, 3, 5, noise_pmax=0.2)),
+    }
+
+
 def main():
     assert oracle.ref_available(), "build the reference first: make -C oracle ref"
     out = []
@@ -116,6 +126,10 @@ def main():
     vec["dist_n8_k2_s77_state"] = st
     vec["dist_n8_k2_s77_bytes"] = byts
     vec["dist_n8_k2_s77_msgs"] = msgs
+    # Precision::Single (complex64): tiled (13 qubits; a 6-qubit density
+    # matrix = 12 flat qubits) and small-state workloads
+    for name, (n, density, c) in single_workloads().items():
+        vec[name] = oracle.ref_run_single(n, to_oracle_ops(c), density=density)
     np.savez_compressed(HERE / "ref_vectors.npz", **vec)
     print(f"wrote {len(out)} KATs and {len(vec)} reference vectors")
 

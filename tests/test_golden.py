@@ -104,3 +104,37 @@ def test_product_distributed_vector_loopback():
         q.destroy()
     finally:
         env.destroy()
+
+
+def _single_workloads():
+    import importlib.util
+
+    spec = importlib.util.spec_from_file_location("make_golden", GOLD / "make_golden.py")
+    mg = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(mg)
+    return mg.single_workloads()
+
+
+@pytest.mark.parametrize("name", ["sp_layered_n13_d5_s3", "sp_random_n5_s99", "sp_dm_noisy_n6_d3_s5"])
+def test_oracle_reproduces_single_precision_vectors(name):
+    """The float restatement reproduces the reference's Precision::Single
+    outputs committed in tests/golden (complex64, bit for bit)."""
+    n, density, c = _single_workloads()[name]
+    assert VEC[name].dtype == np.complex64
+    assert np.array_equal(oracle.orc_run_f(n, to_oracle_ops(c), density), VEC[name])
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["sp_layered_n13_d5_s3", "sp_random_n5_s99", "sp_dm_noisy_n6_d3_s5"])
+def test_product_reproduces_single_precision_vectors(name):
+    from paper_1802_08032_b200 import quest
+
+    n, density, c = _single_workloads()[name]
+    env = quest.Env()
+    try:
+        q = quest.QuregHandle(env, n, density, precision="single")
+        C.run_circuit(q, c)
+        assert np.array_equal(q.state(), VEC[name].astype(np.complex128))
+        q.destroy()
+    finally:
+        env.destroy()
