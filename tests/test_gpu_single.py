@@ -242,3 +242,38 @@ def test_single_smallest_registers_and_empty_circuits(env, n, density):
         assert_parity_f(q.state(), want_single(c, density))
     finally:
         q.destroy()
+
+
+@pytest.mark.parametrize("n", [9, 14])
+def test_single_collapse_measure_and_purity(env, n):
+    """collapseToOutcome / measure on float registers (tiled and small): the
+    kept half is scaled by the narrowed 1/sqrt(P), the rest zeroed; the norm
+    returns to 1 within float rounding. Purity of a float density matrix
+    accumulates in double."""
+    c = random_gate_circuit(n, 80, seed=31 + n, max_controls=1)
+    want = want_single(c).astype(np.complex128)
+    q = quest.QuregHandle(env, n, precision="single")
+    try:
+        C.run_circuit(q, c)
+        idx = np.arange(1 << n)
+        ps = [float(np.sum(np.abs(want[((idx >> k) & 1) == 1]) ** 2)) for k in range(n)]
+        t = int(np.argmax([min(x, 1 - x) for x in ps]))  # the most mixed qubit
+        sel = ((idx >> t) & 1) == 1
+        p = ps[t]
+        got_p = q.collapseToOutcome(t, 1)
+        assert abs(got_p - p) < 1e-12
+        exp = np.where(sel, want * np.float32(1.0 / np.sqrt(p)), 0)
+        assert np.max(np.abs(q.state() - exp)) < 1e-6
+        assert abs(q.calcTotalProb() - 1.0) < 1e-5
+        o = q.measure(2)
+        assert o in (0, 1) and abs(q.calcProbOfOutcome(2, o) - 1.0) < 1e-5
+    finally:
+        q.destroy()
+    d = quest.QuregHandle(env, 5, density=True, precision="single")
+    try:
+        dc = random_gate_circuit(5, 60, seed=8, max_controls=1, channels=True)
+        C.run_circuit(d, dc)
+        rho = want_single(dc, density=True).astype(np.complex128)
+        assert abs(d.calcPurity() - float(np.sum(np.abs(rho) ** 2))) < 1e-12
+    finally:
+        d.destroy()
