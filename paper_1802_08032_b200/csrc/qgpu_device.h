@@ -148,6 +148,7 @@ enum TileCode : uint8_t {
     TC_DEPHASE = 49,
     TC_COLLAPSE = 50,
     TC_DEPOL = 51, // + register-bit pair (0,1) (0,2) (0,3) (1,2) (1,3) (2,3): 51..56
+    TC_DEPOL_LANE = 57, // + register bit of t+N, t on a lane bit: 57..60
 };
 
 // Op header packed in one 64-bit word (one constant-bank load per op):

@@ -289,8 +289,12 @@ bool QuregImpl::place_tile_depol(const FlatOp& op) {
         if (q >= kLaneQubits && !has(tile_high, q)) ++new_high;
     if (static_cast<int>(tile_high.size()) + new_high > env->tile_targets) return false;
     PhaseState* ph = &phases.back();
+    // register qubits it needs: both, or only t+N when t is a fixed lane bit
+    std::vector<int> regq;
+    if (op.q0 >= lane_fixed()) regq.push_back(op.q0);
+    regq.push_back(op.q1);
     int need = 0;
-    for (int q : {op.q0, op.q1})
+    for (int q : regq)
         if (!has(ph->regs, q)) ++need;
     if (static_cast<int>(ph->regs.size()) + need > kPhaseRegBits) {
         if (static_cast<int>(phases.size()) >= max_phases()) return false;
@@ -299,7 +303,7 @@ bool QuregImpl::place_tile_depol(const FlatOp& op) {
         phases.push_back(next);
         ph = &phases.back();
     }
-    for (int q : {op.q0, op.q1}) {
+    for (int q : regq) {
         if (!has(ph->regs, q)) ph->regs.push_back(q);
         if (q >= kLaneQubits && !has(tile_high, q)) tile_high.push_back(q);
     }
@@ -359,8 +363,9 @@ void QuregImpl::enqueue_phys(const FlatOp& op) {
     if (op.kind == FK_DEPOL) {
         // fused into the tile pass when both qubits can be register qubits
         // of a phase (not lane-only qubits 0-2); else its own pass
-        const bool fusable = use_tile() && env->fusion_mode == 0 && op.q0 >= lane_fixed() &&
-                             op.q1 >= lane_fixed() && op.q0 < local_qubits && op.q1 < local_qubits;
+        // (t on a fixed lane bit: the lane variant, TC_DEPOL_LANE)
+        const bool fusable = use_tile() && env->fusion_mode == 0 && op.q1 >= lane_fixed() &&
+                             op.q0 < local_qubits && op.q1 < local_qubits;
         if (!fusable) {
             flush_pass();
             run_depol(op);
@@ -763,7 +768,9 @@ void QuregImpl::launch_tile() {
             // codes), outer controls skip the op per tile
             const bool ctrl = lane_cm != 0 || reg_cm != 0 || warp_cm != 0;
             uint32_t code;
-            if (op.kind == FK_DEPOL) {
+            if (op.kind == FK_DEPOL && q0k == TL_LANE && q1k == TL_REG) {
+                code = TC_DEPOL_LANE + q1p;
+            } else if (op.kind == FK_DEPOL) {
                 if (q0k != TL_REG || q1k != TL_REG)
                     throw DeviceError("internal: a fused depolarising channel needs register qubits");
                 const int j0 = std::min(q0p, q1p), j1 = std::max(q0p, q1p);
