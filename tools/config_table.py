@@ -35,6 +35,7 @@ p = argparse.ArgumentParser()
 p.add_argument("--only", default="C1,C2,C3a,C4,C5")
 p.add_argument("--no-cpu", action="store_true")
 p.add_argument("--cpu-ops", type=int, default=24)
+p.add_argument("--precision", choices=["double", "single"], default="double")
 p.add_argument("--out", default=None)
 a = p.parse_args()
 
@@ -49,7 +50,7 @@ CONFIGS = {
 
 def gpu_time(cfg, c, batch=False):
     env = quest.Env()
-    q = quest.QuregHandle(env, cfg["n"], cfg["density"])
+    q = quest.QuregHandle(env, cfg["n"], cfg["density"], precision=a.precision)
     stream = torch.cuda.ExternalStream(env.stream)
     extra = None
 
@@ -99,7 +100,7 @@ def cpu_time(cfg, c):
         return None, None
     ops = to_oracle_ops(C.Circuit(c.num_qubits, c.depth, c.ops[: a.cpu_ops]))
     workers = os.cpu_count() or 1
-    secs = oracle.ref_time_ops(cfg["n"], ops, workers, 3, density=cfg["density"])
+    secs = oracle.ref_time_ops(cfg["n"], ops, workers, 3, density=cfg["density"], single=a.precision == "single")
     return statistics.median(secs[1:]) / len(ops) * 1e3, workers
 
 
@@ -110,8 +111,9 @@ for name in a.only.split(","):
     flat = 2 * cfg["n"] if cfg["density"] else cfg["n"]
     gates = sum(1 for op in c.ops if op.name not in ("DEPHASE", "DEPOL"))
     ms, norm, extra = gpu_time(cfg, c)
-    B = 2.0 * 16 * 2.0 ** flat
-    row = {"config": name, "qubits": cfg["n"], "density": cfg["density"], "flat_qubits": flat, "ops": len(c.ops),
+    B = 2.0 * (8 if a.precision == "single" else 16) * 2.0 ** flat
+    row = {"config": name, "precision": a.precision, "qubits": cfg["n"], "density": cfg["density"],
+           "flat_qubits": flat, "ops": len(c.ops),
            "gates": gates, "ms_per_step": round(ms, 3), "ms_per_op": round(ms / len(c.ops), 4),
            "effective_TBps": round(B * len(c.ops) / (ms / 1e3) / 1e12, 2), "norm_after": norm}
     if extra:
@@ -131,7 +133,8 @@ for name in a.only.split(","):
 print("\n| config | state | ops | ms/step | ms/op | effective | CPU ref ms/op | x |")
 print("|---|---|---|---|---|---|---|---|")
 for r in rows:
-    st = f"{'DM ' if r['density'] else ''}{r['qubits']}q ({2 ** r['flat_qubits'] * 16 / 2 ** 30:g} GiB)"
+    amp = 8 if r["precision"] == "single" else 16
+    st = f"{'DM ' if r['density'] else ''}{r['qubits']}q ({2 ** r['flat_qubits'] * amp / 2 ** 30:g} GiB)"
     print(f"| {r['config']} | {st} | {r['ops']} | {r['ms_per_step']} | {r['ms_per_op']} | {r['effective_TBps']} TB/s | "
           f"{r.get('cpu_ref_ms_per_op', '—')} | {r.get('speedup_vs_cpu', '—')} |")
 if a.out:
