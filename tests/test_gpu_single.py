@@ -277,3 +277,27 @@ def test_single_collapse_measure_and_purity(env, n):
         assert abs(d.calcPurity() - float(np.sum(np.abs(rho) ** 2))) < 1e-12
     finally:
         d.destroy()
+
+
+@pytest.mark.slow
+def test_single_34q_max_size_forward_inverse(env):
+    """The largest single-precision register one B200 holds (34 qubits, 2^34
+    amplitudes, 128 GiB; qgpuDeviceMaxQubits(single)): a layered circuit and
+    its inverse return to |0> within float rounding, probabilities and the
+    norm through the double-accumulated reductions."""
+    n = 34
+    free, _ = __import__("torch").cuda.mem_get_info()
+    if free < quest.device_bytes_per_rank(n, 0, single=True):
+        pytest.skip("not enough free HBM for 2^34 float amplitudes")
+    c = C.layered_random_circuit(n, 2, 777)
+    q = quest.QuregHandle(env, n, precision="single")
+    try:
+        C.run_circuit(q, c)
+        assert abs(q.calcTotalProb() - 1.0) < 1e-4
+        assert abs(q.calcProbOfOutcome(n - 1, 0) - 0.5) < 0.5
+        C.run_circuit(q, C.inverse_circuit(c))
+        a0 = q.getAmp(0)
+        assert abs(a0.real - 1.0) < 1e-4 and abs(a0.imag) < 1e-4
+        assert abs(q.calcProbOfOutcome(n - 1, 0) - 1.0) < 1e-4
+    finally:
+        q.destroy()
