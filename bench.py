@@ -153,6 +153,15 @@ def circuit_for(n: int, depth: int, seed: int):
     return C.layered_random_circuit(n, depth, seed)
 
 
+def _traffic(key: str, local_qubits: int):
+    """ncu DRAM bytes of one tile-pass launch (profiles/traffic.json)."""
+    try:
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())[key]
+        return t["bytes"] if t["local_qubits"] == local_qubits else None
+    except Exception:
+        return None
+
+
 def effective_bytes(n: int, gates: int) -> float:
     return gates * 2.0 * AMP * (2.0 ** n)
 
@@ -300,7 +309,8 @@ def run_ours(args):
     pk, src = peaks()
     traffic = None
     try:
-        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())["k_tile_pass"]
+        t = json.loads((ROOT / "profiles" / "traffic.json").read_text())[
+            "k_tile_pass_single" if AMP == 8 else "k_tile_pass"]
         if t["local_qubits"] == args.local_qubits and t.get("amp_bytes", 16) == AMP:
             traffic = t["bytes"]
     except Exception:
@@ -369,6 +379,7 @@ def run_ours(args):
               "unit": UNIT, "ms_per_gate": round(t_sp / (gates * args.steps), 4), "dtype": "c64 (f32 pairs)",
               "roofline_frac": round(b_sp / (float(p_s.mean()) / 1e3) / 1e9 / pk["hbm_gbs"], 4) if p_s.size else None,
               "avg_launch_ms": round(float(p_s.mean()), 4) if p_s.size else None,
+              "traffic": _traffic("k_tile_pass_single", args.local_qubits),
               "norm_error": abs(qs.calcTotalProb() - 1.0)}
         qs.destroy()
 
