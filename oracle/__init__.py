@@ -101,6 +101,9 @@ def ref():
         L.ref_partition_info.argtypes = [ctypes.c_int] * 4 + [ctypes.POINTER(ctypes.c_int)] * 2
         L.ref_enumerate_pairs.argtypes = [ctypes.c_int, ctypes.c_int, _vp]
         L.ref_time_ops.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _dp]
+        L.ref_parse_serialize.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
+        L.ref_serialize_random.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong, ctypes.c_char_p, ctypes.c_int,
+                                           ctypes.POINTER(ctypes.c_int)]
         L.ref_time_ops_prec.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _dp]
     return _ref_lib
 
@@ -217,6 +220,24 @@ def ref_rotation_matrix(axis, angle: float) -> np.ndarray:
     m = np.zeros(8)
     _check(ref().ref_rotation_matrix(float(axis[0]), float(axis[1]), float(axis[2]), angle, _ptr(m)))
     return m
+
+
+def ref_parse_serialize(text: str) -> str:
+    """serialize(parse(text)) by the reference (circuit.cpp:123-237); raises
+    OracleError (code 4, the reference's "line N: ..." message) on a parse error."""
+    cap = 64 + 4 * len(text) + (1 << 16)
+    buf = ctypes.create_string_buffer(cap)
+    n = ctypes.c_int(0)
+    _check(ref().ref_parse_serialize(text.encode(), buf, cap, ctypes.byref(n)))
+    return buf.value.decode()
+
+
+def ref_serialize_random(nq: int, depth: int, seed: int) -> str:
+    cap = 64 * (nq * depth + nq + 16) + 64
+    buf = ctypes.create_string_buffer(cap)
+    n = ctypes.c_int(0)
+    _check(ref().ref_serialize_random(nq, depth, seed, buf, cap, ctypes.byref(n)))
+    return buf.value.decode()
 
 
 def ref_reductions(nq: int, amps: np.ndarray, density: bool = False):

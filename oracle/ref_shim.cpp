@@ -363,4 +363,31 @@ int ref_time_ops(int num_qubits, int density, int nops, const orc_op* ops,
     return ref_time_ops_prec(num_qubits, density, 0, nops, ops, workers, reps, seconds);
 }
 
+// Text format (circuit.cpp:123-237): parse `text` with the reference parser
+// and write serialize() of the result to `out` (NUL-terminated; *len = its
+// length). A parse error returns REF_PARSE with the reference's message
+// ("line N: ...") in ref_last_error.
+int ref_parse_serialize(const char* text, char* out, int cap, int* len) {
+    return guarded([&] {
+        const std::string s = qsim::serialize(qsim::parse(text));
+        *len = static_cast<int>(s.size());
+        if (static_cast<int>(s.size()) + 1 > cap)
+            throw qsim::DomainError("output buffer too small");
+        std::memcpy(out, s.c_str(), s.size() + 1);
+    });
+}
+
+// serialize(generate_random_circuit(...)) (circuit.cpp:50-100, 123-136).
+int ref_serialize_random(int num_qubits, int depth, unsigned long long seed, char* out, int cap,
+                         int* len) {
+    return guarded([&] {
+        const std::string s = qsim::serialize(
+            qsim::generate_random_circuit({num_qubits, depth, seed, qsim::Topology::Linear}));
+        *len = static_cast<int>(s.size());
+        if (static_cast<int>(s.size()) + 1 > cap)
+            throw qsim::DomainError("output buffer too small");
+        std::memcpy(out, s.c_str(), s.size() + 1);
+    });
+}
+
 } // extern "C"

@@ -4,7 +4,7 @@ Workload plumbing around the hot path:
 
 * ``gate_matrix`` / ``rotation_matrix`` restate gates.cpp:51-98 with the same
   expressions, so the doubles equal the reference's (pinned in
-  tests/test_circuits.py against the compiled reference).
+  tests/test_host_pins.py against the compiled reference).
 * ``reference_random_circuit`` restates the reference generator
   (circuit.cpp:16-100: SplitMix64, H layer, period-3 CZ pattern, T/SX/SY with
   the first-T and no-repeat rules).
@@ -20,7 +20,9 @@ Workload plumbing around the hot path:
 from __future__ import annotations
 
 import math
+import re
 from dataclasses import dataclass, field
+from fractions import Fraction
 
 MASK64 = (1 << 64) - 1
 
@@ -234,6 +236,13 @@ class ParseError(ValueError):
     pass
 
 
+def _format_angle(x: float) -> str:
+    """circuit.cpp:104-110: printf("%.17g"); glibc prints a NaN's sign."""
+    if math.isnan(x):
+        return "-nan" if math.copysign(1.0, x) < 0 else "nan"
+    return "%.17g" % x
+
+
 def serialize(circuit: Circuit) -> str:
     """circuit.cpp:123-136 (reference gate set only)."""
     lines = [f"qubits {circuit.num_qubits} depth {circuit.depth}"]
@@ -242,18 +251,86 @@ def serialize(circuit: Circuit) -> str:
             raise ValueError(f"gate {op.name} has no text form")
         parts = [op.name, str(op.target), *map(str, op.controls)]
         if op.name in HAS_ANGLE:
-            parts.append("%.17g" % float(op.angle))
+            parts.append(_format_angle(float(op.angle)))
         lines.append(" ".join(parts))
     return "\n".join(lines) + "\n"
 
 
+# std::from_chars<int> (circuit.cpp:144-151): optional '-', ASCII digits, int32
+_INT_RE = re.compile(r"-?[0-9]+")
+# std::stod = strtod's longest prefix (circuit.cpp:153-167): hex, decimal,
+# inf/infinity, nan(n-char-sequence); ERANGE (overflow, or a tiny inexact
+# result) -> out_of_range; no prefix -> invalid_argument; a prefix shorter
+# than the token -> "expected a number"
+_STOD_RES = (
+    re.compile(r"[+-]?0[xX](?:[0-9a-fA-F]+\.?[0-9a-fA-F]*|\.[0-9a-fA-F]+)(?:[pP][+-]?[0-9]+)?"),
+    re.compile(r"[+-]?(?:[0-9]+\.?[0-9]*|\.[0-9]+)(?:[eE][+-]?[0-9]+)?"),
+    re.compile(r"[+-]?inf(?:inity)?", re.IGNORECASE),
+    re.compile(r"[+-]?nan(?:\([0-9A-Za-z_]*\))?", re.IGNORECASE),
+)
+_DBL_MIN = Fraction(2) ** -1022
+
+
+def _exact_hex(tok: str) -> Fraction:
+    sign = -1 if tok[0] == "-" else 1
+    body = tok.lstrip("+-")[2:]
+    mant, _, exp = body.replace("P", "p").partition("p")
+    whole, _, frac = mant.partition(".")
+    digits = whole + frac
+    return sign * Fraction(int(digits, 16)) * Fraction(2) ** (int(exp or 0) - 4 * len(frac))
+
+
+def _parse_int(tok: str, line: int) -> int:
+    if not _INT_RE.fullmatch(tok) or not -(1 << 31) <= int(tok) < (1 << 31):
+        raise ParseError(f"line {line}: expected an integer, got '{tok}'")
+    return int(tok)
+
+
+def _parse_double(tok: str, line: int) -> float:
+    m = None
+    for r in _STOD_RES:
+        m = r.match(tok)
+        if m:
+            break
+    if not m:
+        raise ParseError(f"line {line}: expected a number, got '{tok}'")
+    pre = m.group(0)
+    low = pre.lower().lstrip("+-")
+    erange = False
+    if low.startswith("inf") or low.startswith("nan"):
+        value = float(pre.split("(")[0])
+    else:
+        hexa = low.startswith("0x")
+        exact = _exact_hex(pre) if hexa else Fraction(pre)
+        try:
+            value = float.fromhex(pre) if hexa else float(pre)
+        except OverflowError:
+            value, erange = math.inf, True
+        if math.isinf(value):
+            erange = True
+        elif exact != 0 and abs(exact) < _DBL_MIN and Fraction(value) != exact:
+            erange = True
+    if erange:
+        raise ParseError(f"line {line}: number out of range: '{tok}'")
+    if len(pre) != len(tok):
+        raise ParseError(f"line {line}: expected a number, got '{tok}'")
+    return value
+
+
 def parse(text: str) -> Circuit:
-    """circuit.cpp:172-237."""
+    """circuit.cpp:172-237: std::getline lines ('\\n' only), tokens split on
+    C-locale whitespace, '#' starts a comment only at a token's start; the
+    reference's messages and check order."""
     circuit = None
+    lines = text.split("\n")
+    if lines and lines[-1] == "":
+        lines.pop()
     line_no = 0
-    for line_no, line in enumerate(text.splitlines(), 1):
+    for line_no, line in enumerate(lines, 1):
         toks = []
-        for t in line.split():
+        for t in re.split(r"[ \t\n\v\f\r]+", line):
+            if not t:
+                continue
             if t.startswith("#"):
                 break
             toks.append(t)
@@ -262,10 +339,8 @@ def parse(text: str) -> Circuit:
         if circuit is None:
             if len(toks) != 4 or toks[0] != "qubits" or toks[2] != "depth":
                 raise ParseError(f"line {line_no}: expected header 'qubits N depth D'")
-            try:
-                n, d = int(toks[1]), int(toks[3])
-            except ValueError:
-                raise ParseError(f"line {line_no}: expected an integer") from None
+            n = _parse_int(toks[1], line_no)
+            d = _parse_int(toks[3], line_no)
             if n < 1:
                 raise ParseError(f"line {line_no}: qubit count must be positive")
             circuit = Circuit(n, d, [])
@@ -276,13 +351,10 @@ def parse(text: str) -> Circuit:
         angled = name in HAS_ANGLE
         if len(toks) < 2 or (angled and len(toks) < 3):
             raise ParseError(f"line {line_no}: missing operands for {name}")
-        try:
-            target = int(toks[1])
-            ctrl_end = len(toks) - (1 if angled else 0)
-            controls = tuple(int(t) for t in toks[2:ctrl_end])
-            angle = float(toks[-1]) if angled else 0.0
-        except ValueError:
-            raise ParseError(f"line {line_no}: expected a number") from None
+        target = _parse_int(toks[1], line_no)
+        ctrl_end = len(toks) - (1 if angled else 0)
+        controls = tuple(_parse_int(t, line_no) for t in toks[2:ctrl_end])
+        angle = _parse_double(toks[-1], line_no) if angled else 0.0
         if not 0 <= target < circuit.num_qubits:
             raise ParseError(f"line {line_no}: target {target} out of range for {circuit.num_qubits} qubits")
         for c in controls:

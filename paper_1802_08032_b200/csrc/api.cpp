@@ -532,6 +532,8 @@ int qgpuGetPrecision(Qureg qureg) {
 Qureg createCloneQureg(Qureg qureg, QuESTEnv env) {
     return guarded("createCloneQureg", null_qureg(), [&] {
         QuregImpl* src = reg_of(qureg);
+        if (env_of(env) != src->env) // shards are copied one to one (same ranks, same stream)
+            throw qgpu::DomainError("createCloneQureg needs the environment the source register lives in");
         QuregImpl* r = create_register(env_of(env), src->N, src->density, src->single);
         src->flush();
         r->sp = src->sp; // same logical -> physical qubit map
@@ -601,7 +603,8 @@ void initZeroState(Qureg qureg) {
 void initPlusState(Qureg qureg) {
     guarded_void("initPlusState", [&] {
         QuregImpl* r = reg_of(qureg);
-        r->discard();
+        r->discard_all(); // queued logical ops are dead too (lq), not just the open pass
+        r->sp.reset(r->flat, r->local_qubits, r->env->chunk_amps); // uniform state: any layout
         const double v = r->density ? 1.0 / static_cast<double>(uint64_t{1} << r->N)
                                     : 1.0 / std::sqrt(static_cast<double>(uint64_t{1} << r->N));
         for (auto& s : r->shards) launch_fill(s.amps, r->single, r->local_len, v, 0.0, r->env->stream);
@@ -657,7 +660,12 @@ void initStateFromAmps(Qureg qureg, qreal* reals, qreal* imags) {
         QuregImpl* r = reg_of(qureg);
         require_statevec(r, "initStateFromAmps");
         if (!reals || !imags) throw qgpu::DomainError("null amplitude arrays");
-        r->discard();
+        const uint64_t len = uint64_t{1} << r->flat;
+        for (uint64_t i = 0; i < len; ++i) // validate before any mutation (register.cpp:46-47)
+            if (!std::isfinite(reals[i]) || !std::isfinite(imags[i]))
+                throw qgpu::DomainError("amplitude must be finite");
+        r->discard_all(); // the whole state is rewritten: drop queued ops and the qubit permutation
+        r->sp.reset(r->flat, r->local_qubits, r->env->chunk_amps);
         set_amps_impl(r, 0, reals, imags, nullptr, static_cast<long long>(uint64_t{1} << r->flat));
     });
 }

@@ -347,7 +347,11 @@ void QuregImpl::drain(size_t count) {
             run_swap(p, v);
             sp.apply(p, v);
         };
-        if (need0[i] >= 0) make_local(need0[i], 0);
+        // a channel's second qubit that is already local must not be evicted
+        // to make room for the first (it would be swapped straight back)
+        uint64_t busy0 = 0;
+        if (need1[i] >= 0 && sp.l2p[need1[i]] < local_qubits) busy0 = uint64_t{1} << sp.l2p[need1[i]];
+        if (need0[i] >= 0) make_local(need0[i], busy0);
         if (need1[i] >= 0) make_local(need1[i], uint64_t{1} << sp.l2p[need0[i]]);
         FlatOp op = lop;
         op.q0 = sp.phys(lop.q0);

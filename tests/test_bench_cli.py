@@ -52,8 +52,26 @@ def test_random_circuit_records():
                      if op.target >= 8 and not (op.name in ("Z", "CZ", "RZ", "PHASE", "T", "S")))
     recs = bench_cli.bench_random_circuit(10, 10, 3, ranks_log2=2, strategy="full_clone", reps=3, warmup=1)
     assert len({r["comm_messages"] for r in recs}) == 1
-    # controls on rank bits make some ranks skip: at most 4 messages per gate
-    assert 0 < recs[0]["comm_messages"] <= 4 * comm_gates
+    # exact count: one message per rank per communicated gate, minus the
+    # ranks whose rank-bit controls fail (they skip the gate without traffic,
+    # distributed.cpp:141-145); diagonal gates (T, CZ) never exchange here
+    local = 8
+
+    def passing_ranks(op):
+        return sum(1 for r in range(4)
+                   if all((r >> (cq - local)) & 1 for cq in op.controls if cq >= local))
+
+    exact = sum(passing_ranks(op) for op in c.ops if op.target >= local and op.name not in ("T", "CZ", "Z"))
+    assert recs[0]["comm_messages"] == exact
+    assert recs[0]["comm_bytes"] == exact * 16 * (1 << local)
+    import oracle
+
+    if oracle.ref_available():  # the reference's own count (every global target exchanges)
+        from tests.harness import to_oracle_ops
+
+        _, msgs, byts, _ = oracle.ref_run_distributed(10, to_oracle_ops(c), 2, "full_clone")
+        assert int(msgs.sum()) == sum(passing_ranks(op) for op in c.ops if op.target >= local)
+        assert int(byts.sum()) == int(msgs.sum()) * 16 * (1 << local)
     swap = bench_cli.bench_random_circuit(10, 10, 3, ranks_log2=2, strategy="swap", reps=2, warmup=1)
     assert swap[0]["comm_bytes"] < recs[0]["comm_bytes"]
 

@@ -593,3 +593,79 @@ def test_nccl_environment_single_rank(precision):
         q.destroy()
     finally:
         e.destroy()
+
+
+def _product_matrix(env, apply):
+    """The 2x2 matrix a C-ABI gate call applies, read off a 1-qubit register:
+    column j = the state after the gate on |j> (pair_lo_out / pair_hi_out
+    with a unit and a zero amplitude reproduce the coefficients exactly)."""
+    cols = []
+    for j in (0, 1):
+        q = quest.QuregHandle(env, 1)
+        try:
+            q.initClassicalState(j)
+            apply(q)
+            cols.append(q.state())
+        finally:
+            q.destroy()
+    (m00, m10), (m01, m11) = cols
+    return [m00.real, m00.imag, m01.real, m01.imag, m10.real, m10.imag, m11.real, m11.imag]
+
+
+@pytest.mark.skipif(not oracle.ref_available(), reason="compiled reference not present")
+def test_product_gate_matrices_equal_reference(env):
+    """hadamard / pauliX/Y/Z / tGate / rotateX/Y/Z / rotateAroundAxis through
+    the C-ABI apply exactly the reference's gate_matrix / rotation_matrix
+    (gates.cpp:51-98) on random angles and unit axes."""
+    ids = C.REF_GATE_IDS
+    fixed = {"H": "hadamard", "X": "pauliX", "Y": "pauliY", "Z": "pauliZ", "T": "tGate"}
+    for name, fn in fixed.items():
+        got = _product_matrix(env, lambda q: getattr(q, fn)(0))
+        assert got == list(oracle.ref_gate_matrix(ids[name])), name
+    rng = np.random.default_rng(98)
+    for a in list(rng.uniform(-4 * np.pi, 4 * np.pi, 12)) + [0.0, np.pi]:
+        a = float(a)
+        for name in ("RX", "RY", "RZ"):
+            got = _product_matrix(env, lambda q: getattr(q, "rotate" + name[1])(0, a))
+            assert got == list(oracle.ref_gate_matrix(ids[name], a)), (name, a)
+        v = rng.normal(size=3)
+        v /= np.linalg.norm(v)
+        got = _product_matrix(env, lambda q: q.rotateAroundAxis(0, a, quest.Vector(*map(float, v))))
+        assert got == list(oracle.ref_rotation_matrix(v, a)), (v, a)
+
+
+@pytest.mark.parametrize("init", ["initPlusState", "initStateFromAmps"])
+def test_init_after_queued_gates_on_swapping_ranks(init):
+    """Gates queued for swap planning (loopback ranks, qubit swaps on) are
+    dropped by a whole-state initialiser, not applied on top of it."""
+    lb = quest.Env.loopback(4)
+    try:
+        n = 8
+        q = quest.QuregHandle(lb, n)
+        for t in (7, 6, 0, 7):  # 6, 7 are global qubits: these wait in the swap window
+            q.hadamard(t)
+        q.rotateX(6, 0.3)
+        if init == "initPlusState":
+            q.initPlusState()
+            want = np.full(1 << n, 1 / 16, dtype=np.complex128)
+        else:
+            rng = np.random.default_rng(3)
+            want = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
+            quest.call("initStateFromAmps", q.h, np.ascontiguousarray(want.real).ctypes.data,
+                       np.ascontiguousarray(want.imag).ctypes.data)
+        assert np.array_equal(q.state(), want)
+        assert q.getAmp(200) == complex(want[200])
+        q.destroy()
+    finally:
+        lb.destroy()
+
+
+def test_clone_needs_the_source_environment(env):
+    q = quest.QuregHandle(env, 5)
+    other = quest.Env.loopback(2)
+    try:
+        with pytest.raises(quest.DomainError):
+            quest.call("createCloneQureg", q.h, other.h)
+    finally:
+        other.destroy()
+        q.destroy()
