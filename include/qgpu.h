@@ -35,6 +35,10 @@ void qgpuClearError(void);
 const char* qgpuVersion(void);
 /* Kernel launches issued by the library since load. */
 unsigned long long qgpuKernelLaunches(void);
+/* Host<->device bytes since load: explicit copies (amplitude reads/writes,
+ * reduction results) plus the op tables the pass kernels receive as launch
+ * parameters. Either pointer may be NULL. */
+void qgpuTransferBytes(unsigned long long* h2d, unsigned long long* d2h);
 /* HBM passes / exchange rounds executed for this register. */
 unsigned long long qgpuPassCount(Qureg qureg);
 /* Launch every queued op of this register now (stream-ordered, async). */
@@ -55,6 +59,9 @@ int qgpuGetDevice(QuESTEnv env);
  * 3 depolarise, 4 reduce). */
 void qgpuProfileStart(QuESTEnv env);
 int qgpuProfileStop(QuESTEnv env, double* ms, int* kinds, int maxRecords);
+/* Per-record detail of the last profile window (same order as
+ * qgpuProfileStop): fused tile passes carry ops | phases << 16. */
+int qgpuProfileInfo(QuESTEnv env, int* info, int maxRecords);
 
 /* ------------------------------------------------------------- precision */
 /* Register(num_qubits, kind, precision) (register.hpp:53-54): precision 1 =
@@ -111,6 +118,25 @@ QuESTEnv qgpuCreateLoopbackEnv(int numRanks);
  * qgpuGetNcclUniqueId and distributes the 128 bytes. */
 int qgpuGetNcclUniqueId(char* out128);
 QuESTEnv qgpuCreateNcclEnv(int rank, int numRanks, int device, const char* uniqueId128);
+/* One process per GPU of one node over peer memory (the default multi-GPU
+ * transport; replaces Transport / InProcessTransport, transport.hpp:18-62):
+ * every rank maps every rank's partition (CUDA IPC over NVLink/NVSwitch);
+ * an exchange gate, a depolarising channel on a global bra qubit or a
+ * global<->local qubit swap is one kernel per rank that updates its half of
+ * the amplitude pairs in both partitions in place (no staging buffer, no
+ * send/recv). Rank 0 calls qgpuPeerUniqueId (it creates the group's
+ * shared-memory control segment) and distributes the 128 bytes; every rank
+ * then calls qgpuCreatePeerEnv. A rank that exits, aborts or stalls past
+ * QGPU_PEER_TIMEOUT_S makes its partners' calls fail with
+ * QGPU_COMM_ERROR instead of hanging. */
+int qgpuPeerUniqueId(char* out128);
+QuESTEnv qgpuCreatePeerEnv(int rank, int numRanks, int device, const char* id128);
+/* Host-only self test of a peer group's control plane (no GPU): attach as
+ * `rank`, run `rounds` checked all-gathers and barriers; exitAfter >= 0
+ * makes this process exit mid-protocol at that round (failure-detection
+ * tests). Returns 0, or QGPU_COMM_ERROR with the reason in
+ * qgpuGetLastError. */
+int qgpuPeerProbe(const char* id128, int rank, int numRanks, int rounds, int exitAfter);
 /* Exchange sub-chunk size in amplitudes (power of two, default 2^24). */
 void qgpuSetExchangeChunk(QuESTEnv env, long long int amps);
 /* Global<->local qubit swaps (default on): a gate whose target is a global

@@ -104,6 +104,8 @@ def ref():
         L.ref_parse_serialize.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.c_int, ctypes.POINTER(ctypes.c_int)]
         L.ref_serialize_random.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_ulonglong, ctypes.c_char_p, ctypes.c_int,
                                            ctypes.POINTER(ctypes.c_int)]
+        L.ref_time_distributed.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int,
+                                           ctypes.c_int, _dp, ctypes.POINTER(ctypes.c_ulonglong)]
         L.ref_time_ops_prec.argtypes = [ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp, ctypes.c_int, ctypes.c_int, _dp]
     return _ref_lib
 
@@ -220,6 +222,17 @@ def ref_rotation_matrix(axis, angle: float) -> np.ndarray:
     m = np.zeros(8)
     _check(ref().ref_rotation_matrix(float(axis[0]), float(axis[1]), float(axis[2]), angle, _ptr(m)))
     return m
+
+
+def ref_time_distributed(nq: int, ops, k: int, workers: int, reps: int, strategy: str = "full_clone"):
+    """Seconds of the reference's run_gate_ops (its own clock) per rep, and
+    the bytes its ranks sent in one rep."""
+    ops = as_ops(ops)
+    secs = (ctypes.c_double * reps)()
+    b = ctypes.c_ulonglong(0)
+    _check(ref().ref_time_distributed(nq, k, STRATEGIES[strategy], len(ops), _ptr(ops), workers, reps, secs,
+                                      ctypes.byref(b)))
+    return list(secs), b.value
 
 
 def ref_parse_serialize(text: str) -> str:

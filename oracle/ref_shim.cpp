@@ -390,4 +390,32 @@ int ref_serialize_random(int num_qubits, int depth, unsigned long long seed, cha
     });
 }
 
+// Distributed CPU baseline: the reference's own
+// run_gate_ops over InProcessTransport with one thread per rank, timed by
+// the reference itself (gate_seconds: clock started once all ranks are
+// ready, stopped after the final global barrier, distributed.cpp:323-352).
+// Allocation and zero-init are outside the clock; `reps` repetitions.
+int ref_time_distributed(int num_qubits, int k, int strategy, int nops, const orc_op* ops, int workers,
+                         int reps, double* seconds, unsigned long long* bytes_sent) {
+    return guarded([&] {
+        auto plan = qsim::partition(num_qubits, k, static_cast<qsim::Strategy>(strategy));
+        std::vector<qsim::FlatGateOp> flat_ops;
+        for (int i = 0; i < nops; ++i) {
+            if (ops[i].kind != ORC_GATE) throw qsim::DomainError("distributed engine runs gates only");
+            const auto controls = mask_to_controls(ops[i].ctrl_mask);
+            flat_ops.push_back({qsim::detail::make_control_mask(num_qubits, controls, ops[i].target),
+                                ops[i].target, to_matrix(ops[i])});
+        }
+        auto ranks = qsim::make_ranks(plan, qsim::Precision::Double);
+        qsim::InProcessTransport transport(plan.rank_count());
+        for (int r = 0; r < reps; ++r) {
+            qsim::init_ranks_zero(ranks);
+            double secs = 0.0;
+            const auto stats = qsim::run_gate_ops(ranks, plan, flat_ops, transport, workers, nullptr, &secs);
+            seconds[r] = secs;
+            if (bytes_sent) *bytes_sent = stats.total_bytes();
+        }
+    });
+}
+
 } // extern "C"

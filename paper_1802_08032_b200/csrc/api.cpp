@@ -11,6 +11,7 @@
 
 #include "qgpu_kernels.h"
 #include "runtime.h"
+#include "peer.h"
 #include "transport.h"
 
 #include <algorithm>
@@ -50,6 +51,17 @@ void report(int code, const std::string& msg, const char* func) {
         invalidQuESTInputError(t_msg.c_str(), func);
 }
 
+// A transport or device failure inside a collective leaves the partner
+// ranks blocked; fail them fast instead: peer groups get the message
+// (their barriers throw CommError), NCCL communicators are aborted.
+void abort_groups(const std::string& msg) {
+    std::lock_guard<std::mutex> lk(g_live_mu);
+    for (Env* e : g_envs) {
+        if (e->peer) e->peer->abort("rank " + std::to_string(e->rank) + ": " + msg);
+        if (e->nccl) e->nccl->abort();
+    }
+}
+
 template <class F, class R>
 R guarded(const char* func, R fallback, F&& f) {
     t_code = QGPU_OK;
@@ -61,8 +73,10 @@ R guarded(const char* func, R fallback, F&& f) {
     } catch (const qgpu::ResourceError& e) {
         report(QGPU_RESOURCE_ERROR, e.what(), func);
     } catch (const qgpu::CommError& e) {
+        abort_groups(std::string(func) + ": " + e.what());
         report(QGPU_COMM_ERROR, e.what(), func);
     } catch (const qgpu::DeviceError& e) {
+        abort_groups(std::string(func) + ": " + e.what());
         report(QGPU_DEVICE_ERROR, e.what(), func);
     } catch (const std::bad_alloc&) {
         report(QGPU_RESOURCE_ERROR, "host allocation failed", func);
@@ -266,6 +280,34 @@ uint64_t fold_seeds(const uint64_t* seeds, int n) {
     return st;
 }
 
+// Rank 0's value of `v` on every rank (one all-gather of 8 bytes).
+uint64_t agree_on_rank0(Env* e, uint64_t v) {
+    if (e->num_ranks <= 1) return v;
+    std::vector<uint64_t> all(static_cast<size_t>(e->num_ranks));
+    if (e->mode == Mode::Peer) {
+        e->peer->allgather(&v, all.data(), sizeof(v));
+        return all[0];
+    }
+    if (e->mode == Mode::Nccl) {
+        uint64_t* d = nullptr;
+        cuda_check(cudaMalloc(&d, sizeof(uint64_t) * (all.size() + 1)), "cudaMalloc");
+        try {
+            cuda_check(memcpy_counted(d, &v, sizeof(v), cudaMemcpyHostToDevice, e->stream), "seed");
+            e->nccl->allgather(d, d + 1, sizeof(v), e->stream);
+            cuda_check(memcpy_counted(all.data(), d + 1, sizeof(v) * all.size(), cudaMemcpyDeviceToHost,
+                                       e->stream),
+                       "seed");
+            cuda_check(cudaStreamSynchronize(e->stream), "seed");
+        } catch (...) {
+            cudaFree(d);
+            throw;
+        }
+        cudaFree(d);
+        return all[0];
+    }
+    return v;
+}
+
 QuESTEnv make_env(Mode mode, int rank, int nranks, int device, const char* id128) {
     if (nranks < 1 || (nranks & (nranks - 1)))
         throw qgpu::DomainError("rank count must be a power of two, got " +
@@ -291,6 +333,10 @@ QuESTEnv make_env(Mode mode, int rank, int nranks, int device, const char* id128
     if (const char* v = std::getenv("QGPU_TILE_PHASES"))
         e->tile_phases = std::clamp(std::atoi(v), 1, qgpu::kMaxPhases);
     if (mode == Mode::Nccl && nranks > 1) e->nccl = std::make_unique<NcclComm>(rank, nranks, id128);
+    if (mode == Mode::Peer) e->peer = std::make_unique<qgpu::PeerGroup>(rank, nranks, device, id128);
+    // measure() draws its outcome from this state on every rank: all ranks
+    // must hold rank 0's seed (QuEST broadcasts its default seed)
+    e->rng = agree_on_rank0(e.get(), e->rng);
     QuESTEnv out;
     out.rank = mode == Mode::Loopback ? 0 : rank;
     out.numRanks = nranks;
@@ -308,7 +354,7 @@ Qureg make_handle(QuregImpl* r) {
     q.numQubitsInStateVec = r->flat;
     q.numAmpsPerChunk = static_cast<long long>(r->local_len);
     q.numAmpsTotal = static_cast<long long>(uint64_t{1} << r->flat);
-    q.chunkId = r->env->mode == Mode::Nccl ? r->env->rank : 0;
+    q.chunkId = r->env->multi_process() ? r->env->rank : 0;
     q.numChunks = r->env->num_ranks;
     q.impl = r;
     {
@@ -355,7 +401,10 @@ void enqueue_collapse(QuregImpl* r, int t, int outcome, double prob) {
     op.q1 = r->density ? t + r->N : -1;
     op.outcome = static_cast<uint8_t>(outcome);
     op.m[0] = r->density ? 1.0 / prob : 1.0 / std::sqrt(prob);
-    r->enqueue(op);
+    if (r->density)
+        r->enqueue(op);
+    else
+        r->defer_collapse(op); // fused into the next pass; reductions select around it
 }
 
 } // namespace
@@ -391,6 +440,13 @@ const char* qgpuVersion(void) { return "qgpu 0.1 (sm_100a)"; }
 
 unsigned long long qgpuKernelLaunches(void) { return qgpu::launch_count(); }
 
+void qgpuTransferBytes(unsigned long long* h2d, unsigned long long* d2h) {
+    uint64_t a = 0, b = 0;
+    qgpu::transfer_bytes(&a, &b);
+    if (h2d) *h2d = a;
+    if (d2h) *d2h = b;
+}
+
 // ------------------------------------------------------------- environment
 
 QuESTEnv createQuESTEnv(void) {
@@ -417,6 +473,40 @@ QuESTEnv qgpuCreateNcclEnv(int rank, int numRanks, int device, const char* uniqu
                    [&] { return make_env(Mode::Nccl, rank, numRanks, device, uniqueId128); });
 }
 
+int qgpuPeerUniqueId(char* out128) {
+    return guarded("qgpuPeerUniqueId", 1, [&] {
+        if (!out128) throw qgpu::DomainError("null id buffer");
+        qgpu::PeerGroup::unique_id(out128);
+        return 0;
+    });
+}
+
+QuESTEnv qgpuCreatePeerEnv(int rank, int numRanks, int device, const char* id128) {
+    QuESTEnv bad{0, 0, nullptr};
+    return guarded("qgpuCreatePeerEnv", bad, [&] {
+        if (!id128) throw qgpu::DomainError("null peer group id");
+        return make_env(Mode::Peer, rank, numRanks, device, id128);
+    });
+}
+
+int qgpuPeerProbe(const char* id128, int rank, int numRanks, int rounds, int exitAfter) {
+    return guarded("qgpuPeerProbe", static_cast<int>(QGPU_COMM_ERROR), [&] {
+        if (!id128) throw qgpu::DomainError("null peer group id");
+        qgpu::PeerGroup g(rank, numRanks, 0, id128, false);
+        for (int it = 0; it < rounds; ++it) {
+            if (it == exitAfter) std::_Exit(3); // a rank that dies mid-protocol
+            const uint64_t mine = static_cast<uint64_t>(rank) * 1000003u + static_cast<uint64_t>(it);
+            std::vector<uint64_t> all(static_cast<size_t>(numRanks));
+            g.allgather(&mine, all.data(), sizeof(mine));
+            for (int r = 0; r < numRanks; ++r)
+                if (all[r] != static_cast<uint64_t>(r) * 1000003u + static_cast<uint64_t>(it))
+                    throw qgpu::CommError("peer mailbox mismatch at round " + std::to_string(it));
+            if (it % 7 == 0) g.barrier();
+        }
+        return 0;
+    });
+}
+
 void destroyQuESTEnv(QuESTEnv env) {
     guarded_void("destroyQuESTEnv", [&] {
         Env* e = env_of(env);
@@ -433,8 +523,9 @@ void syncQuESTEnv(QuESTEnv env) {
     guarded_void("syncQuESTEnv", [&] {
         Env* e = env_of(env);
         for (QuregImpl* q : e->quregs) q->flush();
-        cuda_check(cudaStreamSynchronize(e->stream), "syncQuESTEnv");
+        e->wait_stream(e->stream);
         cuda_check(cudaStreamSynchronize(e->comm_stream), "syncQuESTEnv");
+        if (e->peer) e->peer->barrier(); // every rank's work finished (QuEST: MPI_Barrier)
     });
 }
 
@@ -445,7 +536,10 @@ void reportQuESTEnv(QuESTEnv env) {
         Env* e = env_of(env);
         cudaDeviceProp p;
         cuda_check(cudaGetDeviceProperties(&p, e->device), "cudaGetDeviceProperties");
-        const char* mode = e->mode == Mode::Single ? "single" : e->mode == Mode::Loopback ? "loopback" : "nccl";
+        const char* mode = e->mode == Mode::Single     ? "single"
+                           : e->mode == Mode::Loopback ? "loopback"
+                           : e->mode == Mode::Peer     ? "peer"
+                                                       : "nccl";
         std::printf("EXECUTION ENVIRONMENT:\nRunning on %s (sm_%d%d, %d SMs), %s mode, rank %d of %d\n",
                     p.name, p.major, p.minor, p.multiProcessorCount, mode, e->rank, e->num_ranks);
         std::printf("Fusion mode %d, max %d ops/pass, %d register qubits\nPrecision: complex double\n",
@@ -468,6 +562,11 @@ void seedQuESTDefault(QuESTEnv* env) {
     unsigned long int seeds[2] = {static_cast<unsigned long>(std::time(nullptr)),
                                   static_cast<unsigned long>(getpid())};
     seedQuEST(env, seeds, 2);
+    guarded_void("seedQuESTDefault", [&] {
+        if (!env) throw qgpu::DomainError("null QuESTEnv");
+        Env* e = env_of(*env);
+        e->rng = agree_on_rank0(e, e->rng); // rank 0's default seed everywhere
+    });
 }
 
 void qgpuSetFusion(QuESTEnv env, int mode, int maxOps, int regQubits) {
@@ -538,7 +637,7 @@ Qureg createCloneQureg(Qureg qureg, QuESTEnv env) {
         src->flush();
         r->sp = src->sp; // same logical -> physical qubit map
         for (size_t k = 0; k < r->shards.size(); ++k)
-            cuda_check(cudaMemcpyAsync(r->shards[k].amps, src->shards[k].amps,
+            cuda_check(memcpy_counted(r->shards[k].amps, src->shards[k].amps,
                                        r->local_len * r->amp_bytes(), cudaMemcpyDeviceToDevice,
                                        src->env->stream),
                        "clone");
@@ -701,7 +800,7 @@ void cloneQureg(Qureg targetQureg, Qureg copyQureg) {
         t->discard_all();
         t->sp = c->sp;
         for (size_t k = 0; k < t->shards.size(); ++k)
-            cuda_check(cudaMemcpyAsync(t->shards[k].amps, c->shards[k].amps,
+            cuda_check(memcpy_counted(t->shards[k].amps, c->shards[k].amps,
                                        t->local_len * t->amp_bytes(), cudaMemcpyDeviceToDevice,
                                        t->env->stream),
                        "cloneQureg");
@@ -1095,6 +1194,16 @@ int qgpuProfileStop(QuESTEnv env, double* ms, int* kinds, int maxRecords) {
             if (ms) ms[i] = t;
             if (kinds) kinds[i] = e->prof[i].kind;
         }
+        return n;
+    });
+}
+
+int qgpuProfileInfo(QuESTEnv env, int* info, int maxRecords) {
+    return guarded("qgpuProfileInfo", -1, [&] {
+        Env* e = env_of(env);
+        const int n = static_cast<int>(e->prof.size());
+        for (int i = 0; i < n && i < maxRecords; ++i)
+            if (info) info[i] = e->prof[i].info;
         return n;
     });
 }

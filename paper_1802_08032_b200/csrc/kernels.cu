@@ -284,6 +284,113 @@ __global__ void k_combine(V* __restrict__ mine, const V* __restrict__ theirs, ui
     }
 }
 
+// ---- peer-memory exchange (single-node transport, peer.h) -----------------
+// One GPU updates BOTH members of each amplitude pair -- its own element in
+// local HBM and the partner's over NVLink (a mapped peer pointer) -- so no
+// element is ever read after its owner overwrote it and no staging copy
+// exists. The two ranks of a pair split the index range in halves. Four
+// independent elements per thread keep enough remote loads in flight.
+constexpr int kPeerIlp = 4;
+
+// distributed.cpp:174-187 with both halves written: lo_side[i] / hi_side[i]
+// are the pair (own_lo rank's element, partner's element) of local index i.
+template <int CLS, class V, class R>
+__global__ void __launch_bounds__(256) k_peer_combine(V* __restrict__ lo_side, V* __restrict__ hi_side,
+                                                      uint64_t begin, uint64_t n, uint64_t low_mask, MatT<R> m) {
+    const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < n; b += kPeerIlp * T) {
+        V lo[kPeerIlp], hi[kPeerIlp];
+        bool ok[kPeerIlp];
+#pragma unroll
+        for (int k = 0; k < kPeerIlp; ++k) {
+            const uint64_t i = begin + b + k * T;
+            ok[k] = b + k * T < n && (i & low_mask) == low_mask;
+            if (ok[k]) {
+                lo[k] = lo_side[i];
+                hi[k] = hi_side[i];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kPeerIlp; ++k) {
+            if (!ok[k]) continue;
+            const uint64_t i = begin + b + k * T;
+            pair_update<CLS>(lo[k], hi[k], m.m);
+            lo_side[i] = lo[k];
+            hi_side[i] = hi[k];
+        }
+    }
+}
+
+// Global<->local qubit swap: element e of the traded half space sits at
+// own[pos(e, side_own)] and remote[pos(e, !side_own)], pos(e, s) = e with bit
+// v set to s; the two are exchanged (pure moves, exact).
+template <class V>
+__global__ void __launch_bounds__(256) k_peer_swap(V* __restrict__ own, V* __restrict__ remote, uint64_t e0,
+                                                   uint64_t n, int v, int side_own) {
+    const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    const uint64_t low = (uint64_t{1} << v) - 1;
+    const uint64_t so = static_cast<uint64_t>(side_own) << v, sr = static_cast<uint64_t>(side_own ^ 1) << v;
+    for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < n; b += kPeerIlp * T) {
+        V x[kPeerIlp], y[kPeerIlp];
+        uint64_t base[kPeerIlp];
+#pragma unroll
+        for (int k = 0; k < kPeerIlp; ++k) {
+            const uint64_t e = e0 + b + k * T;
+            base[k] = ((e & ~low) << 1) | (e & low);
+            if (b + k * T < n) {
+                x[k] = own[base[k] | so];
+                y[k] = remote[base[k] | sr];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kPeerIlp; ++k) {
+            if (b + k * T >= n) continue;
+            own[base[k] | so] = y[k];
+            remote[base[k] | sr] = x[k];
+        }
+    }
+}
+
+// Depolarising with the bra qubit on the rank bits (k_combine_depol's
+// arithmetic): corner pair k = (col0[i], col1[i | 2^t]), i = k with a zero
+// inserted at bit t; both corners mix as fma(swap, other, keep * self).
+template <class V, class R>
+__global__ void __launch_bounds__(256) k_peer_combine_depol(V* __restrict__ col0, V* __restrict__ col1,
+                                                            uint64_t k0, uint64_t n, int t, R keep, R swap) {
+    const uint64_t T = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    for (uint64_t b = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; b < n; b += kPeerIlp * T) {
+        V x[kPeerIlp], y[kPeerIlp];
+        uint64_t idx[kPeerIlp];
+#pragma unroll
+        for (int k = 0; k < kPeerIlp; ++k) {
+            idx[k] = insert_zero_bit(k0 + b + k * T, t);
+            if (b + k * T < n) {
+                x[k] = col0[idx[k]];
+                y[k] = col1[idx[k] | (uint64_t{1} << t)];
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < kPeerIlp; ++k) {
+            if (b + k * T >= n) continue;
+            col0[idx[k]] = V{fma(swap, y[k].x, keep * x[k].x), fma(swap, y[k].y, keep * x[k].y)};
+            col1[idx[k] | (uint64_t{1} << t)] = V{fma(swap, x[k].x, keep * y[k].x), fma(swap, x[k].y, keep * y[k].y)};
+        }
+    }
+}
+
+// amps[i] *= f for the local indices i whose bit t equals `bit`
+template <class V, class R>
+__global__ void k_scale_bit(V* __restrict__ amps, uint64_t half, int t, int bit, R f) {
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < half;
+         k += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const uint64_t i = insert_zero_bit(k, t) | (static_cast<uint64_t>(bit) << t);
+        V a = amps[i];
+        a.x *= f;
+        a.y *= f;
+        amps[i] = a;
+    }
+}
+
 template <class V, class R>
 __global__ void k_combine_depol(V* __restrict__ mine, const V* __restrict__ theirs, uint64_t len,
                                 uint64_t idx0, int t, int own_col, R keep, R swap, R off) {
@@ -406,6 +513,140 @@ __global__ void k_reduce_diag(const V* __restrict__ amps, uint64_t len, uint64_t
     if (threadIdx.x == 0) partials[blockIdx.x] = make_double2(acc.hi, acc.lo);
 }
 
+// ---- all single-qubit marginals in one read (calcProbOfOutcome cache) ----
+// Block iteration = one chunk of 2^13 amplitudes: thread t reads elements
+// t + 256 j (j < 32), so index bits 0-4 are its lane, 5-7 its warp (both
+// fixed per thread), 8-12 the loop counter j, and bits >= 13 the chunk.
+// Per thread: the chunk's sum and five j-bit sums (32 terms, plain) feed
+// double-double accumulators; each warp's chunk sum goes to wsum for the
+// chunk bits (k_marginals_hi). A final kernel merges the per-block partials
+// in a fixed order (deterministic).
+constexpr int kMargChunkBits = 13;
+constexpr int kMargLo = 1 + 5 + 3 + 5; // total, lane bits, warp bits, j bits
+constexpr int kMargHiMax = 36 - kMargChunkBits;
+constexpr int kMargBlocks = 4 * 148;
+constexpr int kMargHiBlocks = 2 * 148;
+
+__device__ __forceinline__ void block_reduce_store(DD v, double2* out) {
+    v = block_reduce(v);
+    if (threadIdx.x == 0) *out = make_double2(v.hi, v.lo);
+    __syncthreads(); // block_reduce's shared scratch is reused by the next call
+}
+
+template <class V>
+__global__ void __launch_bounds__(256) k_marginals(const V* __restrict__ amps, uint64_t nchunks,
+                                                   double* __restrict__ wsum, double2* __restrict__ part) {
+    DD T{0.0, 0.0}, B[5];
+#pragma unroll
+    for (int b = 0; b < 5; ++b) B[b] = DD{0.0, 0.0};
+    const uint32_t lane = threadIdx.x & 31u, warp = threadIdx.x >> 5;
+    for (uint64_t c = blockIdx.x; c < nchunks; c += gridDim.x) {
+        const V* base = amps + (c << kMargChunkBits) + threadIdx.x;
+        V v[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = __ldcs(base + 256 * j);
+        double cs = 0.0, jb[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+            const double x = v[j].x, y = v[j].y;
+            const double p = __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y));
+            cs += p;
+#pragma unroll
+            for (int b = 0; b < 5; ++b)
+                if ((j >> b) & 1) jb[b] += p;
+        }
+        dd_acc(T, cs);
+#pragma unroll
+        for (int b = 0; b < 5; ++b) dd_acc(B[b], jb[b]);
+        double ws = cs;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ws += __shfl_xor_sync(0xffffffffu, ws, o);
+        if (lane == 0) wsum[(c << 3) | warp] = ws;
+    }
+    double2* out = part + static_cast<size_t>(blockIdx.x) * kMargLo;
+    block_reduce_store(T, out);
+#pragma unroll
+    for (int b = 0; b < 5; ++b) block_reduce_store((lane >> b) & 1u ? T : DD{0.0, 0.0}, out + 1 + b);
+#pragma unroll
+    for (int b = 0; b < 3; ++b) block_reduce_store((warp >> b) & 1u ? T : DD{0.0, 0.0}, out + 6 + b);
+#pragma unroll
+    for (int b = 0; b < 5; ++b) block_reduce_store(B[b], out + 9 + b);
+}
+
+// chunk-bit marginals from the per-(chunk, warp) sums: element i of wsum
+// belongs to chunk i >> 3
+__global__ void __launch_bounds__(256) k_marginals_hi(const double* __restrict__ wsum, uint64_t nw, int hib,
+                                                      double2* __restrict__ part) {
+    double acc[kMargHiMax];
+#pragma unroll
+    for (int b = 0; b < kMargHiMax; ++b) acc[b] = 0.0;
+    for (uint64_t i = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; i < nw;
+         i += static_cast<uint64_t>(gridDim.x) * blockDim.x) {
+        const double w = wsum[i];
+        const uint64_t c = i >> 3;
+#pragma unroll
+        for (int b = 0; b < kMargHiMax; ++b)
+            if (b < hib && ((c >> b) & 1u)) acc[b] += w;
+    }
+    double2* out = part + static_cast<size_t>(blockIdx.x) * kMargHiMax;
+    for (int b = 0; b < hib; ++b) block_reduce_store(DD{acc[b], 0.0}, out + b);
+}
+
+// out[0] = total, out[1 + q] = sum over bit q == 1, q < m (double-double)
+__global__ void __launch_bounds__(256) k_marginals_final(const double2* __restrict__ part, int g1,
+                                                         const double2* __restrict__ part2, int g2, int hib,
+                                                         double2* __restrict__ out) {
+    for (int k = 0; k < kMargLo; ++k) {
+        DD a{0.0, 0.0};
+        for (int i = threadIdx.x; i < g1; i += blockDim.x) {
+            const double2 v = part[static_cast<size_t>(i) * kMargLo + k];
+            a = dd_add(a, DD{v.x, v.y});
+        }
+        block_reduce_store(a, out + k); // k: total, bits 0-4, 5-7, 8-12 in order
+    }
+    for (int b = 0; b < hib; ++b) {
+        DD a{0.0, 0.0};
+        for (int i = threadIdx.x; i < g2; i += blockDim.x) {
+            const double2 v = part2[static_cast<size_t>(i) * kMargHiMax + b];
+            a = dd_add(a, DD{v.x, v.y});
+        }
+        block_reduce_store(a, out + kMargLo + b); // bit 13 + b
+    }
+}
+
+// Sum of |a|^2 over the amplitudes whose local index holds `val` on the bits
+// of `mask` (up to 8 bits; the selection reductions of deferred collapses):
+// only the selected 2^-popcount(mask) of the state is read.
+template <class V>
+__global__ void __launch_bounds__(kReduceThreads)
+k_reduce_norm_sel(const V* __restrict__ amps, uint64_t n, uint64_t mask, uint64_t val,
+                  double2* __restrict__ partials) {
+    DD acc{0.0, 0.0};
+    int pos[8];
+    int np = 0;
+    for (uint64_t m = mask; m && np < 8; m &= m - 1) pos[np++] = __ffsll(static_cast<long long>(m)) - 1;
+    const uint64_t stride = static_cast<uint64_t>(gridDim.x) * blockDim.x;
+    auto at = [&](uint64_t k) {
+        for (int j = 0; j < np; ++j) k = insert_zero_bit(k, pos[j]); // ascending positions
+        return k | val;
+    };
+    for (uint64_t k = blockIdx.x * static_cast<uint64_t>(blockDim.x) + threadIdx.x; k < n; k += 4 * stride) {
+        V v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const uint64_t kk = k + u * stride;
+            v[u] = kk < n ? __ldcs(amps + at(kk)) : V{0, 0};
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double x = v[u].x, y = v[u].y;
+            dd_acc(acc, __dadd_rn(__dmul_rn(x, x), __dmul_rn(y, y)));
+        }
+    }
+    acc = block_reduce(acc);
+    if (threadIdx.x == 0) partials[blockIdx.x] = make_double2(acc.hi, acc.lo);
+}
+
 __global__ void k_reduce_final(const double2* __restrict__ partials, int n,
                                double2* __restrict__ result) {
     DD acc{0.0, 0.0};
@@ -428,6 +669,18 @@ uint64_t launch_count() { return g_launches.load(std::memory_order_relaxed); }
 
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
+namespace {
+std::atomic<uint64_t> g_h2d{0}, g_d2h{0};
+}
+void count_transfer(uint64_t h2d, uint64_t d2h) {
+    if (h2d) g_h2d.fetch_add(h2d, std::memory_order_relaxed);
+    if (d2h) g_d2h.fetch_add(d2h, std::memory_order_relaxed);
+}
+void transfer_bytes(uint64_t* h2d, uint64_t* d2h) {
+    *h2d = g_h2d.load(std::memory_order_relaxed);
+    *d2h = g_d2h.load(std::memory_order_relaxed);
+}
+
 void launch_pass(double2* amps, const PassParams& p, cudaStream_t s) {
     constexpr int threads = 256;
     const uint64_t warps = p.num_tiles;
@@ -440,6 +693,7 @@ void launch_pass(double2* amps, const PassParams& p, cudaStream_t s) {
     case 2: k_fused_pass<2><<<static_cast<unsigned>(blocks), threads, 0, s>>>(amps, p); break;
     default: k_fused_pass<3><<<static_cast<unsigned>(blocks), threads, 0, s>>>(amps, p); break;
     }
+    count_transfer(sizeof(PassParams) + sizeof(amps), 0);
     count_launch();
 }
 
@@ -548,6 +802,102 @@ void launch_combine_depol(void* mine, const void* theirs, bool single, uint64_t 
     else
         k_combine_depol<<<g, 256, 0, s>>>(as<double2>(mine), as<double2>(theirs), len, idx0, t, own_col,
                                           keep, swap, off);
+    count_launch();
+}
+
+namespace {
+template <class V, class R>
+void peer_combine(V* lo_side, V* hi_side, uint64_t begin, uint64_t n, uint64_t low_mask, const Mat2& mat,
+                  int cls, cudaStream_t s) {
+    const unsigned g = grid_for((n + kPeerIlp - 1) / kPeerIlp, 256);
+    const MatT<R> m = narrow<R>(mat);
+    switch (cls) {
+    case CLS_REAL: k_peer_combine<CLS_REAL><<<g, 256, 0, s>>>(lo_side, hi_side, begin, n, low_mask, m); break;
+    case CLS_RX: k_peer_combine<CLS_RX><<<g, 256, 0, s>>>(lo_side, hi_side, begin, n, low_mask, m); break;
+    case CLS_SWAP: k_peer_combine<CLS_SWAP><<<g, 256, 0, s>>>(lo_side, hi_side, begin, n, low_mask, m); break;
+    default: k_peer_combine<CLS_GENERIC><<<g, 256, 0, s>>>(lo_side, hi_side, begin, n, low_mask, m); break;
+    }
+}
+} // namespace
+
+void launch_peer_combine(void* lo_side, void* hi_side, bool single, uint64_t begin, uint64_t n,
+                         uint64_t low_mask, const Mat2& m, int cls, cudaStream_t s) {
+    if (n == 0) return;
+    if (single)
+        peer_combine<float2, float>(as<float2>(lo_side), as<float2>(hi_side), begin, n, low_mask, m, cls, s);
+    else
+        peer_combine<double2, double>(as<double2>(lo_side), as<double2>(hi_side), begin, n, low_mask, m, cls, s);
+    count_launch();
+}
+
+void launch_peer_swap(void* own, void* remote, bool single, uint64_t e0, uint64_t n, int v, int side_own,
+                      cudaStream_t s) {
+    if (n == 0) return;
+    const unsigned g = grid_for((n + kPeerIlp - 1) / kPeerIlp, 256);
+    if (single)
+        k_peer_swap<<<g, 256, 0, s>>>(as<float2>(own), as<float2>(remote), e0, n, v, side_own);
+    else
+        k_peer_swap<<<g, 256, 0, s>>>(as<double2>(own), as<double2>(remote), e0, n, v, side_own);
+    count_launch();
+}
+
+void launch_peer_combine_depol(void* col0, void* col1, bool single, uint64_t k0, uint64_t n, int t,
+                               double keep, double swap, cudaStream_t s) {
+    if (n == 0) return;
+    const unsigned g = grid_for((n + kPeerIlp - 1) / kPeerIlp, 256);
+    if (single)
+        k_peer_combine_depol<<<g, 256, 0, s>>>(as<float2>(col0), as<float2>(col1), k0, n, t,
+                                               static_cast<float>(keep), static_cast<float>(swap));
+    else
+        k_peer_combine_depol<<<g, 256, 0, s>>>(as<double2>(col0), as<double2>(col1), k0, n, t, keep, swap);
+    count_launch();
+}
+
+void launch_scale_bit(void* amps, bool single, uint64_t len, int t, int bit, double f, cudaStream_t s) {
+    const uint64_t half = len / 2;
+    const unsigned g = grid_for(half, 256);
+    if (single)
+        k_scale_bit<<<g, 256, 0, s>>>(as<float2>(amps), half, t, bit, static_cast<float>(f));
+    else
+        k_scale_bit<<<g, 256, 0, s>>>(as<double2>(amps), half, t, bit, f);
+    count_launch();
+}
+
+size_t marginals_scratch_bytes(int m) {
+    const uint64_t nw = m >= kMargChunkBits ? (uint64_t{1} << (m - kMargChunkBits)) * 8 : 0;
+    return nw * sizeof(double) + (static_cast<size_t>(kMargBlocks) * kMargLo +
+                                  static_cast<size_t>(kMargHiBlocks) * kMargHiMax) * sizeof(double2);
+}
+
+void launch_marginals(const void* amps, bool single, int m, void* scratch, double2* out, cudaStream_t s) {
+    const uint64_t nchunks = uint64_t{1} << (m - kMargChunkBits);
+    const uint64_t nw = nchunks * 8;
+    double* wsum = static_cast<double*>(scratch);
+    double2* part = reinterpret_cast<double2*>(wsum + nw);
+    double2* part2 = part + static_cast<size_t>(kMargBlocks) * kMargLo;
+    const int g1 = static_cast<int>(std::min<uint64_t>(nchunks, kMargBlocks));
+    const int hib = m - kMargChunkBits;
+    if (single)
+        k_marginals<<<g1, 256, 0, s>>>(as<float2>(amps), nchunks, wsum, part);
+    else
+        k_marginals<<<g1, 256, 0, s>>>(as<double2>(amps), nchunks, wsum, part);
+    const int g2 = static_cast<int>(std::max<uint64_t>(1, std::min<uint64_t>((nw + 255) / 256, kMargHiBlocks)));
+    if (hib > 0) k_marginals_hi<<<g2, 256, 0, s>>>(wsum, nw, hib, part2);
+    k_marginals_final<<<1, 256, 0, s>>>(part, g1, part2, g2, hib, out);
+    count_launch();
+    count_launch();
+    if (hib > 0) count_launch();
+}
+
+void launch_reduce_norm_sel(const void* amps, bool single, uint64_t len, uint64_t mask, uint64_t val,
+                            double2* partials, double2* result, cudaStream_t s) {
+    const uint64_t n = len >> __builtin_popcountll(mask);
+    if (single)
+        k_reduce_norm_sel<<<kReduceBlocks, kReduceThreads, 0, s>>>(as<float2>(amps), n, mask, val, partials);
+    else
+        k_reduce_norm_sel<<<kReduceBlocks, kReduceThreads, 0, s>>>(as<double2>(amps), n, mask, val, partials);
+    k_reduce_final<<<1, kReduceThreads, 0, s>>>(partials, kReduceBlocks, result);
+    count_launch();
     count_launch();
 }
 

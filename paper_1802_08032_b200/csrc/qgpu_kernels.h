@@ -18,6 +18,10 @@ constexpr int kReduceThreads = 256;
 // gpu_launches and the tests' evidence that the CUDA path ran).
 uint64_t launch_count();
 void count_launch(); // internal: every launcher calls it once per kernel
+// Host<->device bytes since load: explicit copies plus the op tables the
+// pass kernels receive as launch parameters (TileParams / PassParams).
+void count_transfer(uint64_t h2d, uint64_t d2h);
+void transfer_bytes(uint64_t* h2d, uint64_t* d2h);
 
 // Fused pass: applies params.ops in order to every amplitude in one HBM
 // read + write (kernels.cu: k_fused_pass).
@@ -73,6 +77,24 @@ void launch_combine_depol(void* mine, const void* theirs, bool single, uint64_t 
                           uint64_t idx0, int t, int own_col, double keep,
                           double swap, double off, cudaStream_t s);
 
+// Peer-memory exchange (single-node transport, peer.h): one rank updates
+// both members of each pair, its own element and its partner's through a
+// mapped peer pointer; the pair's two ranks take halves of the range.
+// Exchange gate on local indices [begin, begin + n): (lo_side[i], hi_side[i])
+// <- G (lo_side[i], hi_side[i]) where (i & low_mask) == low_mask.
+void launch_peer_combine(void* lo_side, void* hi_side, bool single, uint64_t begin, uint64_t n,
+                         uint64_t low_mask, const Mat2& m, int cls, cudaStream_t s);
+// Qubit swap: elements [e0, e0 + n) of the traded half space, own side has
+// bit v == side_own, the remote side the other value; exchanged in place.
+void launch_peer_swap(void* own, void* remote, bool single, uint64_t e0, uint64_t n, int v, int side_own,
+                      cudaStream_t s);
+// Depolarising corner pairs [k0, k0 + n) between the rank whose bra bit is 0
+// (col0) and its partner (col1), t = the ket qubit's local position.
+void launch_peer_combine_depol(void* col0, void* col1, bool single, uint64_t k0, uint64_t n, int t,
+                               double keep, double swap, cudaStream_t s);
+// amps[i] *= f where bit t of local index i == bit
+void launch_scale_bit(void* amps, bool single, uint64_t len, int t, int bit, double f, cudaStream_t s);
+
 // Compensated reductions (double-double accumulation in either precision).
 // result = (hi, lo) double-double on the device.
 // reduce_norm: sum |a_i|^2 over i in [0, len) (global index goff + i) with
@@ -85,6 +107,18 @@ void launch_reduce_norm(const void* amps, bool single, uint64_t len, uint64_t go
 void launch_reduce_diag(const void* amps, bool single, uint64_t len, uint64_t goff, int N,
                         int t, int outcome, int comp, double2* partials,
                         double2* result, cudaStream_t s);
+
+// All single-qubit marginals of a state-vector partition of 2^m amplitudes
+// (m >= 13) in one read: out[0] = sum |a|^2, out[1 + q] = the sum over
+// local index bit q == 1 (double-double, deterministic). `scratch` holds
+// marginals_scratch_bytes(m).
+constexpr int kMarginalsMinQubits = 13;
+size_t marginals_scratch_bytes(int m);
+void launch_marginals(const void* amps, bool single, int m, void* scratch, double2* out, cudaStream_t s);
+// sum |a|^2 over the local indices i with (i & mask) == val (popcount(mask)
+// <= 8): reads only the selected amplitudes
+void launch_reduce_norm_sel(const void* amps, bool single, uint64_t len, uint64_t mask, uint64_t val,
+                            double2* partials, double2* result, cudaStream_t s);
 
 // every amplitude = re + i im (narrowed to float for single)
 void launch_fill(void* amps, bool single, uint64_t len, double re, double im, cudaStream_t s);

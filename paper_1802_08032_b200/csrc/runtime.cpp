@@ -17,15 +17,24 @@
 //                                   density.cpp:147-154 (compensated)
 #include "runtime.h"
 
+#include "peer.h"
 #include "qgpu_kernels.h"
 #include "transport.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
+#include <thread>
 #include <cstdlib>
 #include <cstring>
 
 namespace qgpu {
+
+cudaError_t memcpy_counted(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
+    if (kind == cudaMemcpyHostToDevice) count_transfer(bytes, 0);
+    if (kind == cudaMemcpyDeviceToHost) count_transfer(0, bytes);
+    return cudaMemcpyAsync(dst, src, bytes, kind, s);
+}
 
 void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)
@@ -35,6 +44,7 @@ void cuda_check(cudaError_t e, const char* what) {
 Env::~Env() {
     for (QuregImpl* q : std::vector<QuregImpl*>(quregs.begin(), quregs.end())) delete q;
     nccl.reset();
+    peer.reset();
     for (auto& r : prof) {
         cudaEventDestroy(r.start);
         cudaEventDestroy(r.stop);
@@ -42,6 +52,29 @@ Env::~Env() {
     for (auto e : event_pool) cudaEventDestroy(e);
     if (stream) cudaStreamDestroy(stream);
     if (comm_stream) cudaStreamDestroy(comm_stream);
+}
+
+void Env::wait_stream(cudaStream_t s) {
+    if (!nccl) {
+        cuda_check(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        return;
+    }
+    static const double timeout_s = [] {
+        const char* v = std::getenv("QGPU_NCCL_TIMEOUT_S");
+        return v ? std::max(1.0, std::atof(v)) : 600.0;
+    }();
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+        const cudaError_t e = cudaStreamQuery(s);
+        if (e == cudaSuccess) return;
+        if (e != cudaErrorNotReady) cuda_check(e, "cudaStreamQuery");
+        nccl->check_async();
+        if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+            nccl->abort();
+            throw CommError("rank " + std::to_string(rank) + " timed out waiting for NCCL (QGPU_NCCL_TIMEOUT_S)");
+        }
+        std::this_thread::sleep_for(std::chrono::microseconds(50));
+    }
 }
 
 cudaEvent_t Env::take_event() {
@@ -55,7 +88,7 @@ cudaEvent_t Env::take_event() {
     return e;
 }
 
-ProfScope::ProfScope(Env* env, int kind) : env_(env), kind_(kind) {
+ProfScope::ProfScope(Env* env, int kind, int info) : env_(env), kind_(kind), info_(info) {
     if (!env_->profile) return;
     start_ = env_->take_event();
     cuda_check(cudaEventRecord(start_, env_->stream), "cudaEventRecord");
@@ -65,7 +98,7 @@ ProfScope::~ProfScope() {
     if (!start_) return;
     cudaEvent_t stop = env_->take_event();
     cudaEventRecord(stop, env_->stream);
-    env_->prof.push_back({start_, stop, kind_});
+    env_->prof.push_back({start_, stop, kind_, info_});
 }
 
 uint8_t classify(const double* m, uint8_t* diag_flags) {
@@ -161,6 +194,15 @@ QuregImpl* create_register(Env* env, int N, bool density, bool single) {
         }
         q->shards.push_back(sh);
     }
+    if (env->mode == Mode::Peer) {
+        try {
+            q->peer_amps = env->peer->open_all(q->shards[0].amps);
+        } catch (...) {
+            cudaFree(q->shards[0].amps);
+            q->shards.clear();
+            throw;
+        }
+    }
     const int nresults = std::max(nshards, env->num_ranks) + 1;
     if (cudaMalloc(&q->partials, kReduceBlocks * sizeof(double2)) != cudaSuccess ||
         cudaMalloc(&q->results, nresults * sizeof(double2)) != cudaSuccess) {
@@ -172,7 +214,7 @@ QuregImpl* create_register(Env* env, int N, bool density, bool single) {
     if (q->shards[0].rank == 0) {
         const double2 one = make_double2(1.0, 0.0);
         const float2 one_f = make_float2(1.0f, 0.0f);
-        cuda_check(cudaMemcpyAsync(q->shards[0].amps, single ? static_cast<const void*>(&one_f) : &one,
+        cuda_check(memcpy_counted(q->shards[0].amps, single ? static_cast<const void*>(&one_f) : &one,
                                    q->amp_bytes(), cudaMemcpyHostToDevice, env->stream),
                    "init zero state");
         cuda_check(cudaStreamSynchronize(env->stream), "init zero state");
@@ -185,12 +227,15 @@ QuregImpl::~QuregImpl() {
     if (env) {
         cudaStreamSynchronize(env->stream);
         env->quregs.erase(this);
+        if (env->peer && !peer_amps.empty()) env->peer->close_all(peer_amps); // collective
     }
     for (auto& s : shards) cudaFree(s.amps);
     cudaFree(recv[0]);
     cudaFree(recv[1]);
     cudaFree(partials);
     cudaFree(results);
+    cudaFree(marg_scratch);
+    cudaFree(marg_dev);
 }
 
 void QuregImpl::fill_zero() {
@@ -312,6 +357,8 @@ bool QuregImpl::place_tile_depol(const FlatOp& op) {
 }
 
 void QuregImpl::enqueue(const FlatOp& lop) {
+    materialize();
+    ++version;
     if (!swaps_on()) {
         enqueue_phys(lop);
         return;
@@ -415,8 +462,21 @@ void QuregImpl::enqueue_phys(const FlatOp& op) {
 }
 
 void QuregImpl::flush() {
+    materialize();
     if (!lq.empty()) drain(lq.size());
     flush_pass();
+}
+
+void QuregImpl::defer_collapse(const FlatOp& op) {
+    ++version;
+    deferred.push_back(op);
+}
+
+void QuregImpl::materialize() {
+    if (deferred.empty()) return;
+    std::vector<FlatOp> d;
+    d.swap(deferred);
+    for (const FlatOp& op : d) enqueue(op);
 }
 
 void QuregImpl::flush_pass() {
@@ -833,7 +893,7 @@ void QuregImpl::launch_tile() {
     const uint64_t rank_need = common & ~local_mask;
     P.num_tiles >>= __builtin_popcountll(P.skip_ones);
     if (pass_stats_enabled()) record_pass_stats(P);
-    ProfScope prof(env, PK_PASS);
+    ProfScope prof(env, PK_PASS, P.phases[P.num_phases - 1].op_end | (P.num_phases << 16));
     for (auto& s : shards) {
         P.global_offset = goff(s);
         if ((P.global_offset & rank_need) != rank_need) continue;
@@ -1001,10 +1061,10 @@ static void exchange_rounds(QuregImpl& q, int rank_bit, uint64_t rank_mask, uint
         if ((static_cast<uint64_t>(s.rank) & rank_mask) != rank_mask) continue;
         Shard& p = q.shards[peer];
         for (uint64_t c0 = 0; c0 < q.local_len; c0 += chunk) {
-            cuda_check(cudaMemcpyAsync(q.recv[0], q.at(p.amps, c0), bytes, cudaMemcpyDeviceToDevice,
+            cuda_check(memcpy_counted(q.recv[0], q.at(p.amps, c0), bytes, cudaMemcpyDeviceToDevice,
                                        env->stream),
                        "loopback exchange");
-            cuda_check(cudaMemcpyAsync(q.recv[1], q.at(s.amps, c0), bytes, cudaMemcpyDeviceToDevice,
+            cuda_check(memcpy_counted(q.recv[1], q.at(s.amps, c0), bytes, cudaMemcpyDeviceToDevice,
                                        env->stream),
                        "loopback exchange");
             combine(s, q.at(s.amps, c0), q.recv[0], chunk, c0);
@@ -1022,9 +1082,34 @@ void QuregImpl::run_exchange_gate(const FlatOp& op) {
     const uint64_t rank_mask = op.cmask >> local_qubits;
     const uint64_t low_mask = op.cmask & (local_len - 1);
     const uint64_t chunk = std::min<uint64_t>(env->chunk_amps, local_len);
-    ensure_recv(chunk);
     Mat2 m;
     std::memcpy(m.m, op.m, sizeof(m.m));
+    if (env->mode == Mode::Peer) {
+        // fused exchange + combine over peer memory: the pair (own_lo rank's
+        // element i, partner's element i) is updated by one GPU, each rank
+        // taking half of the local indices; no staging buffer
+        Shard& s = shards[0];
+        const bool active = (static_cast<uint64_t>(s.rank) & rank_mask) == rank_mask; // :141-145
+        const int peer = s.rank ^ (1 << rank_bit);
+        const std::vector<int> wait = active ? std::vector<int>{peer} : std::vector<int>{};
+        env->peer->fence(env->stream, wait); // both partitions quiescent
+        if (active) {
+            ProfScope prof(env, PK_EXCHANGE);
+            const int own_lo = ((s.rank >> rank_bit) & 1) == 0;
+            void* lo_side = own_lo ? s.amps : peer_amps[peer];
+            void* hi_side = own_lo ? peer_amps[peer] : s.amps;
+            const uint64_t half = local_len / 2;
+            launch_peer_combine(lo_side, hi_side, single, own_lo ? 0 : half, own_lo ? half : local_len - half,
+                                low_mask, m, op.cls, env->stream);
+            cuda_check(cudaGetLastError(), "peer exchange combine");
+            s.messages += 1;
+            s.bytes += local_len * amp_bytes();
+        }
+        env->peer->fence(env->stream, wait); // the partner's writes into this partition landed
+        ++passes;
+        return;
+    }
+    ensure_recv(chunk);
     ProfScope prof(env, PK_EXCHANGE);
     exchange_rounds(*this, rank_bit, rank_mask, chunk,
                     [&](Shard& s, void* mine, void* theirs, uint64_t len, uint64_t idx0) {
@@ -1047,6 +1132,26 @@ void QuregImpl::run_depol(const FlatOp& op) {
         return;
     }
     const int rank_bit = op.q1 - local_qubits;
+    if (env->mode == Mode::Peer) {
+        // corner pairs (col-0 rank's element i, col-1 rank's element i | 2^t)
+        // split between the two ranks; each scales its own off-diagonal half
+        Shard& s = shards[0];
+        const int own_col = (s.rank >> rank_bit) & 1;
+        const int peer = s.rank ^ (1 << rank_bit);
+        env->peer->fence(env->stream, {peer});
+        void* col0 = own_col == 0 ? s.amps : peer_amps[peer];
+        void* col1 = own_col == 0 ? peer_amps[peer] : s.amps;
+        const uint64_t pairs = local_len / 2;
+        launch_peer_combine_depol(col0, col1, single, own_col ? pairs / 2 : 0,
+                                  own_col ? pairs - pairs / 2 : pairs / 2, op.q0, keep, swap, env->stream);
+        launch_scale_bit(s.amps, single, local_len, op.q0, own_col ^ 1, off, env->stream);
+        cuda_check(cudaGetLastError(), "peer depolarise");
+        s.messages += 1;
+        s.bytes += pairs * amp_bytes();
+        env->peer->fence(env->stream, {peer});
+        ++passes;
+        return;
+    }
     uint64_t chunk = std::min<uint64_t>(env->chunk_amps, local_len);
     chunk = std::max<uint64_t>(chunk, uint64_t{2} << op.q0);
     ensure_recv(chunk);
@@ -1083,6 +1188,23 @@ void QuregImpl::run_swap(int g, int v) {
         return (hi << (v + 1)) | (static_cast<uint64_t>(side) << v) | lo;
     };
     ProfScope prof(env, PK_SWAP);
+    if (env->mode == Mode::Peer) {
+        // one kernel per rank moves half of the traded pairs both ways over
+        // peer memory (in place, no staging buffer)
+        Shard& s = shards[0];
+        const int a = (s.rank >> j) & 1;
+        const int peer = s.rank ^ (1 << j);
+        env->peer->fence(env->stream, {peer});
+        const uint64_t half = local_len / 2;
+        launch_peer_swap(s.amps, peer_amps[peer], single, a ? half / 2 : 0, a ? half - half / 2 : half / 2, v,
+                         a ^ 1, env->stream);
+        cuda_check(cudaGetLastError(), "peer swap");
+        s.messages += 1;
+        s.bytes += half * amp_bytes();
+        env->peer->fence(env->stream, {peer});
+        ++passes;
+        return;
+    }
     if (env->mode == Mode::Nccl) {
         Shard& s = shards[0];
         const int a = (s.rank >> j) & 1;
@@ -1097,7 +1219,7 @@ void QuregImpl::run_swap(int g, int v) {
             env->nccl->sendrecv(peer, mine, recv[b], bytes, env->comm_stream);
             cuda_check(cudaEventRecord(ev.recv[b], env->comm_stream), "event");
             cuda_check(cudaStreamWaitEvent(env->stream, ev.recv[b], 0), "event");
-            cuda_check(cudaMemcpyAsync(mine, recv[b], bytes, cudaMemcpyDeviceToDevice, env->stream),
+            cuda_check(memcpy_counted(mine, recv[b], bytes, cudaMemcpyDeviceToDevice, env->stream),
                        "swap");
             cuda_check(cudaEventRecord(ev.done[b], env->stream), "event");
             s.messages += 1;
@@ -1112,9 +1234,9 @@ void QuregImpl::run_swap(int g, int v) {
             for (uint64_t u = 0; u < units; ++u) {
                 void* x = at(s.amps, offset(u, 1));
                 void* y = at(p.amps, offset(u, 0));
-                cuda_check(cudaMemcpyAsync(recv[0], x, bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
-                cuda_check(cudaMemcpyAsync(x, y, bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
-                cuda_check(cudaMemcpyAsync(y, recv[0], bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
+                cuda_check(memcpy_counted(recv[0], x, bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
+                cuda_check(memcpy_counted(x, y, bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
+                cuda_check(memcpy_counted(y, recv[0], bytes, cudaMemcpyDeviceToDevice, env->stream), "swap");
                 s.messages += 1;
                 s.bytes += bytes;
                 p.messages += 1;
@@ -1184,14 +1306,26 @@ struct HostDD {
 
 double QuregImpl::combine_results(int n) {
     std::vector<double2> host(std::max(n, env->num_ranks));
+    if (env->mode == Mode::Peer && env->num_ranks > 1) {
+        double2 mine;
+        cuda_check(memcpy_counted(&mine, results, sizeof(double2), cudaMemcpyDeviceToHost, env->stream),
+                   "reduction readback");
+        cuda_check(cudaStreamSynchronize(env->stream), "reduction");
+        env->peer->allgather(&mine, host.data(), sizeof(double2));
+        n = env->num_ranks;
+        HostDD acc;
+        for (int i = 0; i < n; ++i) acc.add(host[i].x, host[i].y); // rank order
+        return acc.hi + acc.lo;
+    }
     if (env->mode == Mode::Nccl && env->num_ranks > 1) {
         env->nccl->allgather(results, results + 1, sizeof(double2), env->stream);
-        cuda_check(cudaMemcpyAsync(host.data(), results + 1, env->num_ranks * sizeof(double2),
+        cuda_check(memcpy_counted(host.data(), results + 1, env->num_ranks * sizeof(double2),
                                    cudaMemcpyDeviceToHost, env->stream),
                    "reduction readback");
         n = env->num_ranks;
+        env->wait_stream(env->stream);
     } else {
-        cuda_check(cudaMemcpyAsync(host.data(), results, n * sizeof(double2),
+        cuda_check(memcpy_counted(host.data(), results, n * sizeof(double2),
                                    cudaMemcpyDeviceToHost, env->stream),
                    "reduction readback");
     }
@@ -1201,7 +1335,133 @@ double QuregImpl::combine_results(int n) {
     return acc.hi + acc.lo;
 }
 
+double QuregImpl::reduce_sel_phys(uint64_t mask, uint64_t val) {
+    ProfScope prof(env, PK_REDUCE);
+    const uint64_t lmask = mask & (local_len - 1);
+    const uint64_t rmask = mask >> local_qubits, rval = val >> local_qubits;
+    for (size_t k = 0; k < shards.size(); ++k) {
+        if ((static_cast<uint64_t>(shards[k].rank) & rmask) != rval) {
+            cuda_check(cudaMemsetAsync(results + k, 0, sizeof(double2), env->stream), "reduce");
+            continue;
+        }
+        launch_reduce_norm_sel(shards[k].amps, single, local_len, lmask, val & lmask, partials, results + k,
+                               env->stream);
+    }
+    cuda_check(cudaGetLastError(), "reduce");
+    return combine_results(static_cast<int>(shards.size()));
+}
+
+bool QuregImpl::marginals_usable() const {
+    static const bool off = [] {
+        const char* v = std::getenv("QGPU_MARGINALS");
+        return v && std::string(v) == "0";
+    }();
+    return !off && !density && local_qubits >= kMarginalsMinQubits && flat <= 63;
+}
+
+void QuregImpl::compute_marginals() {
+    flush();
+    if (marg_version == version) return;
+    const int m = local_qubits;
+    const size_t per = static_cast<size_t>(1 + m);
+    if (!marg_scratch) {
+        const size_t nvec = std::max(shards.size(), static_cast<size_t>(env->num_ranks)) + 1;
+        if (cudaMalloc(&marg_scratch, marginals_scratch_bytes(m)) != cudaSuccess ||
+            cudaMalloc(&marg_dev, nvec * per * sizeof(double2)) != cudaSuccess) {
+            cudaGetLastError();
+            throw ResourceError("failed to allocate the marginals scratch");
+        }
+    }
+    {
+        ProfScope prof(env, PK_REDUCE);
+        for (size_t k = 0; k < shards.size(); ++k)
+            launch_marginals(shards[k].amps, single, m, marg_scratch, marg_dev + k * per, env->stream);
+        cuda_check(cudaGetLastError(), "marginals");
+    }
+    // every rank's vector on every rank, merged in rank order
+    const int nr = env->num_ranks;
+    std::vector<double2> all(static_cast<size_t>(nr) * per);
+    if (env->mode == Mode::Loopback || env->mode == Mode::Single) {
+        cuda_check(memcpy_counted(all.data(), marg_dev, all.size() * sizeof(double2), cudaMemcpyDeviceToHost,
+                                  env->stream),
+                   "marginals");
+        cuda_check(cudaStreamSynchronize(env->stream), "marginals");
+    } else if (env->mode == Mode::Peer) {
+        std::vector<double2> mine(per);
+        cuda_check(memcpy_counted(mine.data(), marg_dev, per * sizeof(double2), cudaMemcpyDeviceToHost, env->stream),
+                   "marginals");
+        cuda_check(cudaStreamSynchronize(env->stream), "marginals");
+        env->peer->allgather(mine.data(), all.data(), per * sizeof(double2));
+    } else {
+        env->nccl->allgather(marg_dev, marg_dev + per, per * sizeof(double2), env->stream);
+        cuda_check(memcpy_counted(all.data(), marg_dev + per, all.size() * sizeof(double2), cudaMemcpyDeviceToHost,
+                                  env->stream),
+                   "marginals");
+        env->wait_stream(env->stream);
+    }
+    struct Acc {
+        double hi = 0.0, lo = 0.0;
+        void add(double2 v) {
+            const double s = hi + v.x, bb = s - hi;
+            const double e = (hi - (s - bb)) + (v.x - bb);
+            const double t = e + lo + v.y;
+            hi = s + t;
+            lo = t - (hi - s);
+        }
+    };
+    std::vector<Acc> phys(static_cast<size_t>(flat) + 1);
+    for (int r = 0; r < nr; ++r) { // rank order
+        const double2* v = all.data() + static_cast<size_t>(r) * per;
+        phys[0].add(v[0]);
+        for (int q = 0; q < m; ++q) phys[1 + q].add(v[1 + q]);
+        for (int g = m; g < flat; ++g)
+            if ((r >> (g - m)) & 1) phys[1 + g].add(v[0]);
+    }
+    marg.assign(static_cast<size_t>(flat) + 1, make_double2(0.0, 0.0));
+    marg[0] = make_double2(phys[0].hi, phys[0].lo);
+    for (int L = 0; L < flat; ++L) {
+        const int P = swaps_on() ? sp.l2p[L] : L;
+        marg[1 + L] = make_double2(phys[1 + P].hi, phys[1 + P].lo);
+    }
+    marg_version = version;
+}
+
 double QuregImpl::reduce_norm(int t, int outcome) {
+    if (!density && !deferred.empty() && lq.empty() && pending.empty()) {
+        // pending collapses as a selection (logical qubits), scaled by their
+        // scale^2; the state in HBM is the pre-collapse one
+        uint64_t m = 0, v = 0;
+        double s2 = 1.0;
+        bool empty = false;
+        for (const FlatOp& op : deferred) {
+            const uint64_t b = uint64_t{1} << op.q0;
+            if ((m & b) && (((v >> op.q0) & 1u) != op.outcome)) empty = true;
+            m |= b;
+            v |= static_cast<uint64_t>(op.outcome) << op.q0;
+            s2 *= op.m[0] * op.m[0];
+        }
+        if (t >= 0) {
+            const uint64_t b = uint64_t{1} << t;
+            if ((m & b) && (((v >> t) & 1u) != static_cast<uint64_t>(outcome))) empty = true;
+            m |= b;
+            v |= static_cast<uint64_t>(outcome) << t;
+        }
+        const uint64_t pm = swaps_on() ? sp.phys_mask(m) : m, pv = swaps_on() ? sp.phys_mask(v) : v;
+        if (__builtin_popcountll(pm & (local_len - 1)) <= 8) {
+            const double r = reduce_sel_phys(pm, pv); // collective: every rank reduces
+            return empty ? 0.0 : r * s2;
+        }
+    }
+    if (t >= 0 && marginals_usable()) {
+        compute_marginals();
+        const double2 p1 = marg[1 + t];
+        if (outcome) return p1.x + p1.y;
+        // total - P(1) in double-double, then rounded
+        const double2 tot = marg[0];
+        const double s = tot.x - p1.x, bb = s - tot.x;
+        const double e = (tot.x - (s - bb)) + (-p1.x - bb);
+        return s + (e + tot.y - p1.y);
+    }
     flush();
     if (swaps_on()) t = sp.phys(t);
     ProfScope prof(env, PK_REDUCE);
@@ -1235,13 +1495,29 @@ void QuregImpl::get_raw(uint64_t start, uint64_t num, void* out) {
     restore_identity();
     flush();
     const uint64_t end = start + num;
-    if (env->mode == Mode::Nccl && env->num_ranks > 1) {
+    if (env->mode == Mode::Peer && env->num_ranks > 1 && num == 1) {
+        // single amplitude: the owner contributes it through the mailboxes
+        const uint64_t lo = goff(shards[0]);
+        const int owner = static_cast<int>(start >> local_qubits);
+        double2 mine = make_double2(0.0, 0.0);
+        if (owner == shards[0].rank) {
+            cuda_check(memcpy_counted(&mine, at(shards[0].amps, start - lo), amp_bytes(), cudaMemcpyDeviceToHost,
+                                       env->stream),
+                       "read");
+            cuda_check(cudaStreamSynchronize(env->stream), "read");
+        }
+        std::vector<double2> all(env->num_ranks);
+        env->peer->allgather(&mine, all.data(), sizeof(double2));
+        std::memcpy(out, &all[owner], amp_bytes());
+        return;
+    }
+    if (env->multi_process() && env->num_ranks > 1) {
         if (num != 1) {
             const uint64_t lo = goff(shards[0]), hi = lo + local_len;
             if (start < lo || end > hi)
                 throw DomainError("bulk reads are limited to this rank's amplitudes [" +
                                   std::to_string(lo) + ", " + std::to_string(hi) + ")");
-            cuda_check(cudaMemcpyAsync(out, at(shards[0].amps, start - lo), num * amp_bytes(),
+            cuda_check(memcpy_counted(out, at(shards[0].amps, start - lo), num * amp_bytes(),
                                        cudaMemcpyDeviceToHost, env->stream),
                        "read");
             cuda_check(cudaStreamSynchronize(env->stream), "read");
@@ -1252,15 +1528,15 @@ void QuregImpl::get_raw(uint64_t start, uint64_t num, void* out) {
         const int owner = static_cast<int>(start >> local_qubits);
         double2 zero = make_double2(0.0, 0.0);
         if (owner == shards[0].rank)
-            cuda_check(cudaMemcpyAsync(results, at(shards[0].amps, start - lo), amp_bytes(),
+            cuda_check(memcpy_counted(results, at(shards[0].amps, start - lo), amp_bytes(),
                                        cudaMemcpyDeviceToDevice, env->stream),
                        "read");
         else
-            cuda_check(cudaMemcpyAsync(results, &zero, sizeof(double2), cudaMemcpyHostToDevice,
+            cuda_check(memcpy_counted(results, &zero, sizeof(double2), cudaMemcpyHostToDevice,
                                        env->stream),
                        "read");
         env->nccl->allgather(results, results + 1, sizeof(double2), env->stream);
-        cuda_check(cudaMemcpyAsync(out, results + 1 + owner, amp_bytes(),
+        cuda_check(memcpy_counted(out, results + 1 + owner, amp_bytes(),
                                    cudaMemcpyDeviceToHost, env->stream),
                    "read");
         cuda_check(cudaStreamSynchronize(env->stream), "read");
@@ -1270,7 +1546,7 @@ void QuregImpl::get_raw(uint64_t start, uint64_t num, void* out) {
         const uint64_t lo = goff(s), hi = lo + local_len;
         const uint64_t a = std::max(lo, start), b = std::min(hi, end);
         if (a >= b) continue;
-        cuda_check(cudaMemcpyAsync(at(out, a - start), at(s.amps, a - lo), (b - a) * amp_bytes(),
+        cuda_check(memcpy_counted(at(out, a - start), at(s.amps, a - lo), (b - a) * amp_bytes(),
                                    cudaMemcpyDeviceToHost, env->stream),
                    "read");
     }
@@ -1280,12 +1556,13 @@ void QuregImpl::get_raw(uint64_t start, uint64_t num, void* out) {
 void QuregImpl::set_raw(uint64_t start, uint64_t num, const void* in) {
     restore_identity();
     flush();
+    ++version;
     const uint64_t end = start + num;
     for (auto& s : shards) {
         const uint64_t lo = goff(s), hi = lo + local_len;
         const uint64_t a = std::max(lo, start), b = std::min(hi, end);
         if (a >= b) continue;
-        cuda_check(cudaMemcpyAsync(at(s.amps, a - lo), at(const_cast<void*>(in), a - start), (b - a) * amp_bytes(),
+        cuda_check(memcpy_counted(at(s.amps, a - lo), at(const_cast<void*>(in), a - start), (b - a) * amp_bytes(),
                                    cudaMemcpyHostToDevice, env->stream),
                    "write");
     }

@@ -27,12 +27,19 @@ struct CommError : std::runtime_error { using std::runtime_error::runtime_error;
 struct DeviceError : std::runtime_error { using std::runtime_error::runtime_error; };
 
 void cuda_check(cudaError_t e, const char* what);
+// cudaMemcpyAsync that adds host<->device bytes to the transfer counters
+// (qgpuTransferBytes: the bench's e2e h2d / d2h bytes per step)
+cudaError_t memcpy_counted(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s);
 
 // ------------------------------------------------------------- transport
 
-class NcclComm; // transport.cpp
+class NcclComm;  // transport.cpp
+class PeerGroup; // peer.cpp
 
-enum class Mode { Single, Loopback, Nccl };
+// Single: one GPU. Loopback: 2^k virtual ranks on one GPU. Nccl: one process
+// per GPU over NCCL send/recv. Peer: one process per GPU of one node, every
+// partition mapped into every rank (CUDA IPC over NVLink; peer.h).
+enum class Mode { Single, Loopback, Nccl, Peer };
 
 struct Env {
     int device = 0;
@@ -60,6 +67,8 @@ struct Env {
     // qgpuSetQubitSwaps turns them off (the reference's exchange per gate)
     bool qubit_swaps = true;
     std::unique_ptr<NcclComm> nccl;
+    std::unique_ptr<PeerGroup> peer;
+    bool multi_process() const { return mode == Mode::Nccl || mode == Mode::Peer; }
     std::set<struct QuregImpl*> quregs;
 
     // Launch profiling (qgpuProfileStart/Stop): an event pair around every
@@ -68,10 +77,15 @@ struct Env {
     struct ProfRec {
         cudaEvent_t start, stop;
         int kind;
+        int info; // PK_PASS: ops | phases << 16
     };
     std::vector<ProfRec> prof;
     std::vector<cudaEvent_t> event_pool;
     cudaEvent_t take_event();
+    // cudaStreamSynchronize that, on NCCL ranks, polls ncclCommGetAsyncError
+    // and gives up after QGPU_NCCL_TIMEOUT_S (a partner that died or threw
+    // would otherwise leave this rank blocked inside NCCL forever)
+    void wait_stream(cudaStream_t s);
 
     ~Env();
 };
@@ -81,12 +95,13 @@ enum ProfKind { PK_PASS = 0, PK_SIMPLE = 1, PK_EXCHANGE = 2, PK_DEPOL = 3, PK_RE
 // Brackets the enclosed launches with an event pair when profiling is on.
 class ProfScope {
   public:
-    ProfScope(Env* env, int kind);
+    ProfScope(Env* env, int kind, int info = 0);
     ~ProfScope();
 
   private:
     Env* env_;
     int kind_;
+    int info_;
     cudaEvent_t start_ = nullptr;
 };
 
@@ -123,6 +138,7 @@ struct QuregImpl {
     int local_qubits = 0;
     uint64_t local_len = 0;
     std::vector<Shard> shards; // 1, or 2^k virtual ranks (Loopback)
+    std::vector<void*> peer_amps; // Peer: every rank's partition mapped here ([rank] = shards[0])
     void* recv[2] = {nullptr, nullptr};
     uint64_t recv_len = 0;
     double2* partials = nullptr; // reduction scratch
@@ -166,8 +182,32 @@ struct QuregImpl {
     void flush();
     void discard_all() { // queued ops are dead (the state is overwritten)
         lq.clear();
+        deferred.clear();
+        ++version;
         discard();
     }
+
+    // ---- measurement support (state vectors)
+    // Every mutation bumps `version`; the single-qubit marginals of the
+    // current state are computed in one read (launch_marginals) and serve
+    // every calcProbOfOutcome / measure until the next mutation.
+    uint64_t version = 0;
+    uint64_t marg_version = ~uint64_t{0};
+    std::vector<double2> marg;       // [0] total, [1 + L] sum over logical qubit L == 1 (double-double)
+    void* marg_scratch = nullptr;    // launch_marginals scratch (lazy)
+    double2* marg_dev = nullptr;     // per-shard / per-rank marginal vectors
+    bool marginals_usable() const;
+    void compute_marginals();
+    // Collapses of a state vector wait here while only reductions follow:
+    // a probability (or the total) is then a reduction over the amplitudes
+    // the pending collapses keep (a fraction of the state) times their
+    // scale^2, and the collapses themselves fuse into the next pass. Any
+    // other op, read or write enqueues them first, in order.
+    std::vector<FlatOp> deferred;    // logical FK_COLLAPSE ops
+    void defer_collapse(const FlatOp& op);
+    void materialize();
+    // sum |a|^2 over the physical selection (mask, val), all shards, rank order
+    double reduce_sel_phys(uint64_t mask, uint64_t val);
     void discard() {
         pending.clear();
         regs.clear();

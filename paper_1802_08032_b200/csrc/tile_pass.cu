@@ -54,6 +54,7 @@ void launch_interp(void (*kern)(T*, TileParams), void* amps, const TileParams& p
 } // namespace
 
 void launch_tile_pass(void* amps, const TileParams& p, cudaStream_t s) {
+    count_transfer(sizeof(TileParams) + sizeof(amps), 0); // the pass's op table rides in the launch
     if (launch_tile_pass_jit(amps, p, s)) { // straight-line kernel for this pass shape
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) throw DeviceError(std::string("jit tile pass launch: ") + cudaGetErrorString(e));

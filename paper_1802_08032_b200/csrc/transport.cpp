@@ -30,6 +30,7 @@ struct NcclApi {
     ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
     ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
     ncclResult_t (*CommAbort)(ncclComm_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     ncclResult_t (*Send)(const void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*Recv)(void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
     ncclResult_t (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
@@ -58,6 +59,7 @@ NcclApi& api() {
         QGPU_BIND(CommInitRank, "ncclCommInitRank");
         QGPU_BIND(CommDestroy, "ncclCommDestroy");
         QGPU_BIND(CommAbort, "ncclCommAbort");
+        QGPU_BIND(CommGetAsyncError, "ncclCommGetAsyncError");
         QGPU_BIND(Send, "ncclSend");
         QGPU_BIND(Recv, "ncclRecv");
         QGPU_BIND(AllGather, "ncclAllGather");
@@ -97,10 +99,30 @@ NcclComm::~NcclComm() {
     if (comm_ && api().CommDestroy) api().CommDestroy(comm_);
 }
 
+void NcclComm::abort() {
+    if (comm_ && api().CommAbort) api().CommAbort(comm_);
+    comm_ = nullptr;
+}
+
+void NcclComm::check_async() {
+    if (!comm_) throw CommError("NCCL communicator of rank " + std::to_string(rank_) + " was aborted");
+    if (!api().CommGetAsyncError) return;
+    ncclResult_t st = 0;
+    const ncclResult_t r = api().CommGetAsyncError(comm_, &st);
+    constexpr ncclResult_t kInProgress = 7; // ncclInProgress
+    if (r != 0 || (st != 0 && st != kInProgress)) {
+        std::string msg = "NCCL asynchronous error on rank " + std::to_string(rank_);
+        if (api().GetErrorString) msg += ": " + std::string(api().GetErrorString(r != 0 ? r : st));
+        abort();
+        throw CommError(msg);
+    }
+}
+
 // One rendezvous exchange (transport.cpp:25-57 semantics: both sides send
 // `bytes` and receive the peer's) as a grouped send/recv on `s`.
 void NcclComm::sendrecv(int peer, const void* send, void* recv, size_t bytes, cudaStream_t s) {
     auto& a = api();
+    if (!comm_) throw CommError("NCCL communicator of rank " + std::to_string(rank_) + " was aborted");
     nccl_check(a.GroupStart(), "ncclGroupStart", rank_, peer);
     nccl_check(a.Send(send, bytes, ncclUint8, peer, comm_, s), "ncclSend", rank_, peer);
     nccl_check(a.Recv(recv, bytes, ncclUint8, peer, comm_, s), "ncclRecv", rank_, peer);
@@ -108,6 +130,7 @@ void NcclComm::sendrecv(int peer, const void* send, void* recv, size_t bytes, cu
 }
 
 void NcclComm::allgather(const void* send, void* recv, size_t bytes, cudaStream_t s) {
+    if (!comm_) throw CommError("NCCL communicator of rank " + std::to_string(rank_) + " was aborted");
     nccl_check(api().AllGather(send, recv, bytes, ncclUint8, comm_, s), "ncclAllGather", rank_, -1);
 }
 

@@ -15,6 +15,11 @@ class NcclComm {
 
     void sendrecv(int peer, const void* send, void* recv, size_t bytes, cudaStream_t s);
     void allgather(const void* send, void* recv, size_t bytes, cudaStream_t s);
+    // ncclCommGetAsyncError: throws CommError (after aborting the
+    // communicator) if NCCL reported an asynchronous failure
+    void check_async();
+    // ncclCommAbort: unblocks this rank's pending NCCL work (idempotent)
+    void abort();
     int rank() const { return rank_; }
     int size() const { return nranks_; }
 

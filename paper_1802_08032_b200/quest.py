@@ -84,6 +84,9 @@ _SIGS = {
     "qgpuCreateLoopbackEnv": (QuESTEnv, [_I]),
     "qgpuCreateNcclEnv": (QuESTEnv, [_I, _I, _I, ctypes.c_char_p]),
     "qgpuGetNcclUniqueId": (_I, [ctypes.c_char_p]),
+    "qgpuCreatePeerEnv": (QuESTEnv, [_I, _I, _I, ctypes.c_char_p]),
+    "qgpuPeerUniqueId": (_I, [ctypes.c_char_p]),
+    "qgpuPeerProbe": (_I, [ctypes.c_char_p, _I, _I, _I, _I]),
     "destroyQuESTEnv": (None, [QuESTEnv]),
     "syncQuESTEnv": (None, [QuESTEnv]),
     "reportQuESTEnv": (None, [QuESTEnv]),
@@ -144,6 +147,7 @@ _SIGS = {
     "qgpuClearError": (None, []),
     "qgpuVersion": (ctypes.c_char_p, []),
     "qgpuKernelLaunches": (_ULL, []),
+    "qgpuTransferBytes": (None, [ctypes.POINTER(ctypes.c_ulonglong), ctypes.POINTER(ctypes.c_ulonglong)]),
     "qgpuPassCount": (_ULL, [Qureg]),
     "qgpuFlush": (None, [Qureg]),
     "qgpuSetFusion": (None, [QuESTEnv, _I, _I, _I]),
@@ -175,6 +179,7 @@ _SIGS = {
     "qgpuJitSelfTest": (_I, [ctypes.c_char_p, _I, ctypes.POINTER(ctypes.c_double)]),
     "qgpuProfileStart": (None, [QuESTEnv]),
     "qgpuProfileStop": (_I, [QuESTEnv, _VP, _VP, _I]),
+    "qgpuProfileInfo": (_I, [QuESTEnv, _VP, _I]),
 }
 
 # Every symbol include/QuEST.h and include/qgpu.h declare.
@@ -238,7 +243,8 @@ def int_array(xs):
 
 class Env:
     """Owns a QuESTEnv. ``Env()`` = one GPU; ``Env.loopback(2**k)`` = 2^k
-    virtual ranks on one GPU; ``Env.nccl(rank, n, device, uid)`` = one
+    virtual ranks on one GPU; ``Env.peer(rank, n, device, uid)`` = one
+    process per GPU of one node over peer memory; ``Env.nccl(rank, n, device, uid)`` = one
     process per GPU."""
 
     def __init__(self, _handle: QuESTEnv | None = None):
@@ -257,6 +263,19 @@ class Env:
     @classmethod
     def nccl(cls, rank: int, num_ranks: int, device: int, uid: bytes) -> "Env":
         return cls(call("qgpuCreateNcclEnv", rank, num_ranks, device, uid))
+
+    @staticmethod
+    def peer_unique_id() -> bytes:
+        """Rank 0 only: creates the peer group's shared-memory control
+        segment and returns its 128-byte id for the other ranks."""
+        buf = ctypes.create_string_buffer(128)
+        call("qgpuPeerUniqueId", buf)
+        return buf.raw
+
+    @classmethod
+    def peer(cls, rank: int, num_ranks: int, device: int, uid: bytes) -> "Env":
+        """One process per GPU of one node over peer memory (qgpu.h)."""
+        return cls(call("qgpuCreatePeerEnv", rank, num_ranks, device, uid))
 
     @property
     def rank(self) -> int:
@@ -301,6 +320,9 @@ class Env:
         kinds = np.zeros(max_records, dtype=np.int32)
         n = call("qgpuProfileStop", self.h, ms.ctypes.data, kinds.ctypes.data, max_records)
         n = min(n, max_records)
+        info = np.zeros(max_records, dtype=np.int32)
+        call("qgpuProfileInfo", self.h, info.ctypes.data, max_records)
+        self.last_info = info[:n].copy()  # fused passes: ops | phases << 16
         return ms[:n].copy(), kinds[:n].copy()
 
     def destroy(self):
@@ -395,6 +417,13 @@ class QuregHandle:
 
     def __exit__(self, *a):
         self.destroy()
+
+
+def transfer_bytes() -> tuple[int, int]:
+    """(host->device, device->host) bytes the library moved since load."""
+    a, b = ctypes.c_ulonglong(0), ctypes.c_ulonglong(0)
+    call("qgpuTransferBytes", ctypes.byref(a), ctypes.byref(b))
+    return a.value, b.value
 
 
 def kernel_launches() -> int:

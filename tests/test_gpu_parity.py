@@ -651,10 +651,11 @@ def test_init_after_queued_gates_on_swapping_ranks(init):
         else:
             rng = np.random.default_rng(3)
             want = rng.normal(size=1 << n) + 1j * rng.normal(size=1 << n)
-            quest.call("initStateFromAmps", q.h, np.ascontiguousarray(want.real).ctypes.data,
-                       np.ascontiguousarray(want.imag).ctypes.data)
+            re, im = np.ascontiguousarray(want.real), np.ascontiguousarray(want.imag)
+            quest.call("initStateFromAmps", q.h, re.ctypes.data, im.ctypes.data)
         assert np.array_equal(q.state(), want)
-        assert q.getAmp(200) == complex(want[200])
+        a = q.getAmp(200)
+        assert complex(a.real, a.imag) == complex(want[200])
         q.destroy()
     finally:
         lb.destroy()
