@@ -116,6 +116,12 @@ constexpr int kTileGroupBits = QGPU_TILE_GROUP_BITS; // independent tile groups 
 constexpr int kTileQubits = kLaneQubits + kPhaseRegBits + kTileWarpBits;
 constexpr int kTileHigh = kTileQubits - kLaneQubits;
 constexpr int kTileThreads = 32 << (kTileWarpBits + kTileGroupBits); // 512 (16 warps)
+// Named barriers (IDs 1..15) of the phase transitions: one CTA-wide group
+// uses them all (its full barrier is __syncthreads, ID 0); with two groups
+// each owns seven, the first being its full-group barrier.
+constexpr int kTileGroups = 1 << kTileGroupBits;
+constexpr int kBarIdsPerGroup = kTileGroups == 1 ? 16 : 15 / kTileGroups; // relative IDs [1, this)
+constexpr int kBarGroupBase = kTileGroups == 1 ? 0 : 1; // group g's ID 0 = kBarGroupBase + g * kBarIdsPerGroup
 // Resident tile-pass CTAs per SM: single precision holds its 8 register
 // amplitudes in 16 registers, so two CTAs (64 registers per thread, 2 x 96 KiB
 // of stages) fit and double the warps that hide shared-memory latency.

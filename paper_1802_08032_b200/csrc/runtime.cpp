@@ -657,17 +657,18 @@ void QuregImpl::launch_tile() {
             ++c;
         sync_bits[p] = c;
     }
-    // named barrier IDs 1..15: each transition its own range of 2^c IDs (a
-    // shared ID let a lagging warp of one transition complete another's
-    // barrier, and mixed thread counts trap); transitions that do not fit
-    // sync the whole CTA
+    // named barrier IDs (per tile group: relative IDs 1 .. kBarIdsPerGroup-1,
+    // qgpu_device.h): each transition its own range of 2^c IDs (a shared ID
+    // let a lagging warp of one transition complete another's barrier, and
+    // mixed thread counts trap); transitions that do not fit sync the whole
+    // group
     std::vector<int> bar_base(nph, 0);
     {
         int next_id = 1;
         for (size_t p = 1; p < nph; ++p) {
             const int c = sync_bits[p];
-            if (c == 0 || c >= kTileWarpBits) continue; // CTA barrier / warp sync
-            if (next_id + (1 << c) > 16) {
+            if (c == 0 || c >= kTileWarpBits) continue; // group barrier / warp sync
+            if (next_id + (1 << c) > kBarIdsPerGroup) {
                 sync_bits[p] = 0;
                 continue;
             }

@@ -15,13 +15,13 @@ namespace qgpu {
 namespace {
 
 template <int RB, int WB, int NBUF>
-__global__ void __launch_bounds__(32 << WB, 1)
+__global__ void __launch_bounds__(kTileThreads, 1)
 k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
     tile_f64::tile_pass_body<RB, WB, NBUF, tile_f64::Interp>(amps, P);
 }
 
 template <int RB, int WB, int NBUF>
-__global__ void __launch_bounds__(32 << WB, kTileCtasF32)
+__global__ void __launch_bounds__(kTileThreads, kTileCtasF32)
 k_tile_pass_f32(float2* __restrict__ amps, const __grid_constant__ TileParams P) {
     tile_f32::tile_pass_body<RB, WB, NBUF, tile_f32::Interp>(amps, P);
 }

@@ -190,11 +190,14 @@ def lib():
     """Load libqgpu.so (raises ImportError if it has not been built)."""
     global _lib
     if _lib is None:
-        if not LIB_PATH.exists():
+        path = LIB_PATH
+        if os.environ.get("QGPU_LIB"):  # an A/B variant build (build.py QGPU_VARIANT)
+            path = Path(os.environ["QGPU_LIB"])
+        if not path.exists():
             raise ImportError(
                 f"{LIB_PATH} is missing: build it with `python -m paper_1802_08032_b200.build` "
                 "(there is no CPU fallback)")
-        L = ctypes.CDLL(str(LIB_PATH))
+        L = ctypes.CDLL(str(path))
         for name, (res, args) in _SIGS.items():
             fn = getattr(L, name)
             fn.restype = res

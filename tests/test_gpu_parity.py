@@ -670,3 +670,48 @@ def test_clone_needs_the_source_environment(env):
     finally:
         other.destroy()
         q.destroy()
+
+
+@pytest.mark.parametrize("ranks", [1, 2, 4])
+@pytest.mark.parametrize("precision", ["double", "single"])
+def test_marginals_and_deferred_collapses(ranks, precision):
+    """calcProbOfOutcome from the one-read marginals (>= 13 local qubits) and
+    collapses deferred as selections: every probability within 1e-12 of the
+    compensated restatement on the state the reference's sequence produces
+    (collapse after collapse), measurement outcomes equal to the restated
+    measure under the same seed, and the final amplitudes."""
+    n = 16
+    c = random_gate_circuit(n, 200, seed=123 + ranks, max_controls=2)
+    env = quest.Env.loopback(ranks) if ranks > 1 else quest.Env()
+    single = precision == "single"
+    tol = 1e-6 if single else TOL
+    try:
+        q = quest.QuregHandle(env, n, precision=precision)
+        C.apply_circuit(q, c)
+        if not single:
+            assert bits_equal(q.state(), oracle_run(c))
+        # the product's state is the checker's input from here on (single
+        # precision: the restatement then works on the widened floats)
+        want = q.state()
+        for t in range(n):
+            for o in (0, 1):
+                assert abs(q.calcProbOfOutcome(t, o) - oracle.orc_prob_of_outcome(want, n, t, o)) < tol
+        cur = want
+        for t, o in [(3, 1), (15, 0), (8, 1), (3, 1), (0, 0)]:
+            p = oracle.orc_prob_of_outcome(cur, n, t, o)
+            assert abs(q.collapseToOutcome(t, o) - p) < tol
+            cur = oracle.orc_collapse(cur, n, t, o, p)
+            for u in (1, 8, 12):
+                assert abs(q.calcProbOfOutcome(u, 1) - oracle.orc_prob_of_outcome(cur, n, u, 1)) < tol
+            assert abs(q.calcTotalProb() - oracle.orc_norm_kahan(cur)) < tol
+        with pytest.raises(quest.DomainError):
+            q.collapseToOutcome(15, 1)  # contradicts a pending collapse: probability 0
+        env.seed(99, 7)
+        st = oracle.orc_seed([99, 7])
+        for t in (5, 9, 14):
+            o, _, cur, st = oracle.orc_measure(cur, n, t, st)
+            assert q.measure(t) == o
+        assert np.max(np.abs(q.state() - cur)) < tol
+        q.destroy()
+    finally:
+        env.destroy()
