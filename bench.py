@@ -495,10 +495,30 @@ def run_ours(args):
         except Exception as e:  # reported, not fatal
             cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
+    # per-pass bound: max(HBM time of the pass's bytes at the measured copy
+    # peak, FP64 time of its modelled instructions at the FP64 pipe's peak:
+    # 148 SMs x 64 DFMA/clk x the max SM clock); the timed passes against
+    # the sum of their bounds
+    bound = None
+    if pass_ms.size:
+        pinfo = info[kinds == 0]
+        fp64_per_amp = (pinfo >> 16) / 4.0
+        fp64_rate = 148 * 64 * 1.965e9  # instructions / s
+        t_hbm = per_launch_bytes / (pk["hbm_gbs"] * 1e9) * 1e3  # ms
+        t_fp = fp64_per_amp * (2.0 ** args.local_qubits) / fp64_rate * 1e3
+        t_bound = np.maximum(t_hbm, t_fp)
+        bound = {"hbm_ms": round(t_hbm, 4), "fp64_ms_mean": round(float(t_fp.mean()), 4),
+                 "fp64_bound_passes": int((t_fp > t_hbm).sum()),
+                 "bound_ms_mean": round(float(t_bound.mean()), 4),
+                 "frac_of_bound": round(float(t_bound.sum() / pass_ms.sum()), 4),
+                 "fp64_model": "per handler class: 8 (generic 2x2), 4 (real / Rx-class / diagonal), 0 (swap) "
+                               "FP64 instructions per amplitude, halved per control outside the tile; "
+                               "peak 148 x 64 DFMA/clk x 1.965 GHz"}
+
     # per-pass-class split: passes by op count, each class's bandwidth
     classes = None
     if pass_ms.size:
-        ops_per_pass = info[kinds == 0] & 0xFFFF
+        ops_per_pass = info[kinds == 0] & 0xFF
         if ops_per_pass.size == pass_ms.size:
             classes = []
             for lo, hi in ((1, 8), (9, 16), (17, 24), (25, 1 << 30)):
@@ -545,7 +565,7 @@ def run_ours(args):
                          "peak_source": src, "bytes_per_launch": per_launch_bytes,
                          "avg_launch_ms": round(float(pass_ms.mean()), 4) if pass_ms.size else None,
                          "launches": int(pass_ms.size), "share_of_step": round(share, 4) if share else None,
-                         "passes_by_op_count": classes},
+                         "per_pass_bound": bound, "passes_by_op_count": classes},
             "clocks": clocks.summary(),
             "check": {"norm_error_after_timed_steps": norm_error},
             "single_gate_pass": single,

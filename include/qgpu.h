@@ -60,7 +60,8 @@ int qgpuGetDevice(QuESTEnv env);
 void qgpuProfileStart(QuESTEnv env);
 int qgpuProfileStop(QuESTEnv env, double* ms, int* kinds, int maxRecords);
 /* Per-record detail of the last profile window (same order as
- * qgpuProfileStop): fused tile passes carry ops | phases << 16. */
+ * qgpuProfileStop): fused tile passes carry ops | phases << 8 | (modelled
+ * FP64 instructions per amplitude x 4) << 16. */
 int qgpuProfileInfo(QuESTEnv env, int* info, int maxRecords);
 
 /* ------------------------------------------------------------- precision */

@@ -88,24 +88,27 @@ struct Mat2 {
 
 // ------------------------------------------------------------ tile pass
 //
-// A CTA owns a tile of 2^kTileQubits amplitudes: the 5 lowest qubits (the
+// A CTA owns tiles of 2^kTileQubits amplitudes: the 5 lowest qubits (the
 // lanes: every warp access is 512 contiguous bytes) plus kTileHigh arbitrary
-// higher qubits. The ops of a pass run in phases; in each phase every thread
-// holds 2^kPhaseRegBits amplitudes in registers spanning 3 of the tile's high
-// qubits (the phase's register qubits), the 16 warps span the other 4. (8
-// amplitudes x 2 ping-pong copies fit 128 registers, so 4 warps per SM
-// sub-partition hide the op dispatch and FP64 latencies; 16 amplitudes per
-// thread left 2 warps per sub-partition and measured 10 % slower.) Gates
-// on lane qubits use warp shuffles, gates on register qubits stay in
-// registers, diagonal ops and channels act elementwise anywhere; between
-// phases the tile is re-laid out through shared memory. Phase 0 loads from
-// HBM and the last phase stores to HBM, so a pass is one read + one write of
-// the state whatever its op count.
+// higher qubits. Its 16 warps form two tile groups of 8 that work on
+// alternate tiles, so one group's phase transitions (shared-memory round
+// trips and barriers) overlap the other group's arithmetic. The ops of a
+// pass run in phases; in each phase every thread of a group holds
+// 2^kPhaseRegBits = 16 amplitudes in registers spanning 4 of the tile's
+// qubits (the phase's register qubits), 2 more ride on lane bits 3-4 and the
+// 8 warps span the remaining 3. Measured on the 30-qubit bench circuit
+// against one group of 16 warps with 8 register amplitudes (3 register
+// qubits): 4 % faster end to end (profiles/r2_tile_groups.md) — most passes
+// need two phases instead of three. Gates on lane qubits use warp shuffles,
+// gates on register qubits stay in registers, diagonal ops and channels act
+// elementwise anywhere; between phases the tile is re-laid out through
+// shared memory. Phase 0 loads from HBM (TMA) and the last phase stores to
+// HBM, so a pass is one read + one write of the state whatever its op count.
 #ifndef QGPU_PHASE_REG_BITS
-#define QGPU_PHASE_REG_BITS 3
+#define QGPU_PHASE_REG_BITS 4
 #endif
 #ifndef QGPU_TILE_GROUP_BITS
-#define QGPU_TILE_GROUP_BITS 0
+#define QGPU_TILE_GROUP_BITS 1
 #endif
 #ifndef QGPU_TILE_WARP_BITS
 #define QGPU_TILE_WARP_BITS (4 - QGPU_TILE_GROUP_BITS)
@@ -120,6 +123,17 @@ constexpr int kTileThreads = 32 << (kTileWarpBits + kTileGroupBits); // 512 (16 
 // uses them all (its full barrier is __syncthreads, ID 0); with two groups
 // each owns seven, the first being its full-group barrier.
 constexpr int kTileGroups = 1 << kTileGroupBits;
+// QGPU_TILE_LDG=1: phase 0 reads HBM straight into registers (coalesced
+// 16-byte loads of tiles prefetched into L2 by cp.async.bulk.prefetch) instead
+// of TMA copies into shared memory; shared memory then only carries the
+// phase transitions (one tile buffer per group), and a one-phase pass does
+// not touch it at all.
+#ifndef QGPU_TILE_LDG
+#define QGPU_TILE_LDG 0
+#endif
+constexpr bool kTileLdg = QGPU_TILE_LDG != 0;
+constexpr int kTileStages = kTileLdg ? (1 << QGPU_TILE_GROUP_BITS) : 3; // shared-memory tile buffers
+constexpr int kTilePrefetch = 2; // LDG mode: tiles per group prefetched into L2 ahead
 constexpr int kBarIdsPerGroup = kTileGroups == 1 ? 16 : 15 / kTileGroups; // relative IDs [1, this)
 constexpr int kBarGroupBase = kTileGroups == 1 ? 0 : 1; // group g's ID 0 = kBarGroupBase + g * kBarIdsPerGroup
 // Resident tile-pass CTAs per SM: single precision holds its 8 register
@@ -220,6 +234,11 @@ struct TileParams {
     uint64_t fin_greg[1 << kPhaseRegBits];
     uint64_t fin_gwarp[1 << kTileWarpBits];
     uint64_t fin_glane[2];
+    // phase 0 under QGPU_TILE_LDG loads straight from HBM: the same offsets
+    // for the first phase's layout
+    uint64_t first_greg[1 << kPhaseRegBits];
+    uint64_t first_gwarp[1 << kTileWarpBits];
+    uint64_t first_glane[2];
     // the 8 segments warp w owns in the last phase (its warp bits fixed)
     uint8_t fin_seg[1 << kTileWarpBits][1 << (kTileHigh - kTileWarpBits)];
     TilePhase phases[kMaxPhases];

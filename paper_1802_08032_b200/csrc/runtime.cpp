@@ -22,6 +22,7 @@
 #include "transport.h"
 
 #include <algorithm>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <thread>
@@ -526,6 +527,51 @@ void record_pass_stats(const TileParams& P) {
     }
 }
 
+// Profile record of a tile pass: ops (bits 0-7), phases (8-15) and a model
+// of the FP64 instructions per amplitude x 4 (16-31) — the reference's fma
+// chain per handler class (8 for a generic 2x2 row pair, 4 for real /
+// Rx-class rows and diagonals, 0 for swaps), halved per control outside the
+// tile (those tiles skip the op) and for a == 1 diagonals on warp / outer
+// qubits (the identity side copies). bench.py turns it into the pass's FP64
+// time bound beside its HBM bound.
+int pass_profile_info(const TileParams& P) {
+    const int nops = P.phases[P.num_phases - 1].op_end;
+    double fp = 0.0;
+    for (int k = 0; k < nops; ++k) {
+        const uint64_t h = P.ops[k].hdr;
+        const int code = static_cast<int>(h & 63);
+        const uint32_t flags = (h >> 6) & 15u;
+        double f;
+        if (code < TC_REG + 16) { // 2x2 on a register bit, by class row
+            const int row = (code - TC_REG) / 4;
+            f = row == 0 ? 8.0 : row == 3 ? 0.0 : 4.0;
+        } else if (code < TC_REG_SEL + 8) {
+            f = (code - TC_REG_SEL) / 4 == 0 ? 8.0 : 0.0;
+        } else if (code == TC_LANE_GENERIC || code == TC_LANE_SEL_GENERIC) {
+            f = 8.0;
+        } else if (code == TC_LANE_REAL) {
+            f = 4.0;
+        } else if (code == TC_LANE_SWAP || code == TC_LANE_SEL_SWAP) {
+            f = 0.0;
+        } else if ((code >= TC_DIAG_REG_D && code < TC_DIAG_REG_D + 4) ||
+                   (code >= TC_DIAG_REG_D_SEL && code < TC_DIAG_REG_D_SEL + 4)) {
+            f = 2.0; // only the bit-1 half
+        } else if (code == TC_DIAG_UNIFORM || code == TC_DIAG_UNIFORM_SEL) {
+            f = (flags & (DF_A_ONE | DF_D_ONE)) ? 2.0 : 4.0;
+        } else if (code == TC_DEPHASE || code == TC_COLLAPSE) {
+            f = 2.0;
+        } else if (code >= TC_DEPOL && code < TC_DEPOL_LANE + 4) {
+            f = 3.0;
+        } else {
+            f = 4.0; // the other diagonals
+        }
+        f *= std::ldexp(1.0, -__builtin_popcountll(P.ops[k].outer_cmask));
+        fp += f;
+    }
+    const int fp4 = std::min(32767, static_cast<int>(fp * 4.0 + 0.5));
+    return nops | (P.num_phases << 8) | (fp4 << 16);
+}
+
 void QuregImpl::launch_tile() {
     // The tile's high qubits: the pass's pair targets, topped up with the
     // lowest unused local qubits (qubits 5, 6, 7 let a warp's last-phase
@@ -736,11 +782,27 @@ void QuregImpl::launch_tile() {
             Q.warp_off[w] = static_cast<uint16_t>(off);
         }
         for (int j = 0; j < 2; ++j) Q.lane_off[j] = static_cast<uint16_t>(1u << lb[j]);
+        auto gbit = [&](int t) -> uint64_t {
+            return t < kLaneQubits ? uint64_t{1} << t : uint64_t{1} << high[t - kLaneQubits];
+        };
+        if (p == 0) {
+            // first phase (LDG mode loads it from HBM): the same offsets
+            for (int i = 0; i < (1 << kPhaseRegBits); ++i) {
+                uint64_t g = 0;
+                for (int j = 0; j < kPhaseRegBits; ++j)
+                    if ((i >> j) & 1) g |= gbit(rb[j]);
+                P.first_greg[i] = g;
+            }
+            for (int w = 0; w < (1 << kTileWarpBits); ++w) {
+                uint64_t g = 0;
+                for (int j = 0; j < kTileWarpBits; ++j)
+                    if ((w >> j) & 1) g |= gbit(wb[j]);
+                P.first_gwarp[w] = g;
+            }
+            for (int j = 0; j < 2; ++j) P.first_glane[j] = gbit(lb[j]);
+        }
         if (p + 1 == phases.size()) {
             // last phase: HBM offsets of its registers, warps and lane bits
-            auto gbit = [&](int t) -> uint64_t {
-                return t < kLaneQubits ? uint64_t{1} << t : uint64_t{1} << high[t - kLaneQubits];
-            };
             for (int i = 0; i < (1 << kPhaseRegBits); ++i) {
                 uint64_t g = 0;
                 for (int j = 0; j < kPhaseRegBits; ++j)
@@ -894,7 +956,7 @@ void QuregImpl::launch_tile() {
     const uint64_t rank_need = common & ~local_mask;
     P.num_tiles >>= __builtin_popcountll(P.skip_ones);
     if (pass_stats_enabled()) record_pass_stats(P);
-    ProfScope prof(env, PK_PASS, P.phases[P.num_phases - 1].op_end | (P.num_phases << 16));
+    ProfScope prof(env, PK_PASS, pass_profile_info(P));
     for (auto& s : shards) {
         P.global_offset = goff(s);
         if ((P.global_offset & rank_need) != rank_need) continue;
@@ -1382,7 +1444,7 @@ void QuregImpl::compute_marginals() {
     // every rank's vector on every rank, merged in rank order
     const int nr = env->num_ranks;
     std::vector<double2> all(static_cast<size_t>(nr) * per);
-    if (env->mode == Mode::Loopback || env->mode == Mode::Single) {
+    if (!env->multi_process() || env->num_ranks == 1) { // every shard in this process
         cuda_check(memcpy_counted(all.data(), marg_dev, all.size() * sizeof(double2), cudaMemcpyDeviceToHost,
                                   env->stream),
                    "marginals");

@@ -61,7 +61,7 @@ void launch_tile_pass(void* amps, const TileParams& p, cudaStream_t s) {
         count_launch();
         return;
     }
-    constexpr int NBUF = 3;
+    constexpr int NBUF = kTileStages;
     if (p.single) {
         static bool set = false;
         launch_interp(k_tile_pass_f32<kPhaseRegBits, kTileWarpBits, NBUF>, amps, p, s,

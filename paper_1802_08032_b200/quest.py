@@ -325,7 +325,7 @@ class Env:
         n = min(n, max_records)
         info = np.zeros(max_records, dtype=np.int32)
         call("qgpuProfileInfo", self.h, info.ctypes.data, max_records)
-        self.last_info = info[:n].copy()  # fused passes: ops | phases << 16
+        self.last_info = info[:n].copy()  # fused passes: ops | phases << 8 | fp64/amp x4 << 16
         return ms[:n].copy(), kinds[:n].copy()
 
     def destroy(self):

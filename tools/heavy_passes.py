@@ -44,7 +44,8 @@ for s in range(a.steps):
         ms, kinds = env.profile_stop()
         info = env.last_info
 ms, info = ms[kinds == 0], info[kinds == 0]
-rows = [{"pass": i, "ms": round(float(t), 4), "ops": int(x & 0xFFFF), "phases": int(x >> 16),
+rows = [{"pass": i, "ms": round(float(t), 4), "ops": int(x & 0xFF), "phases": int((x >> 8) & 0xFF),
+         "fp64_per_amp": (int(x) >> 16) / 4.0,
          "frac": round(bytes_per_pass / (t / 1e3) / 1e9 / 6544.3, 4)} for i, (t, x) in enumerate(zip(ms, info))]
 rows.sort(key=lambda r: -r["ms"])
 print(f"passes/step {ms.size}, total {ms.sum():.2f} ms, mean {ms.mean():.3f} ms")

@@ -7,7 +7,8 @@ OUT=${1:-gpurun_out/heavy}
 mkdir -p "$OUT"
 export QGPU_JIT=sync
 python tools/heavy_passes.py --steps 2 --out "$OUT/passes.json" > "$OUT/passes.txt"
-IDX=$(python -c "import json,sys; r=json.load(open('$OUT/passes.json'))['rows']; print(' '.join(str(x['pass']) for x in r[:3]))")
+# the three longest passes and the median one
+IDX=$(python -c "import json,sys; r=json.load(open('$OUT/passes.json'))['rows']; print(' '.join(str(x['pass']) for x in r[:3] + [r[len(r) // 2]]))")
 echo "top passes: $IDX" >> "$OUT/passes.txt"
 for i in $IDX; do
   timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_tile_jit \
