@@ -100,6 +100,11 @@ def parse_args():
     p.add_argument("--no-c5", action="store_true", help="skip the C5 QFT + measurement side measurement")
     p.add_argument("--jit", type=int, default=None,
                    help="per-pass JIT: 0 off, 1 on (default; env QGPU_JIT=off|sync also applies)")
+    p.add_argument("--order", choices=["reorder", "exact"], default="reorder",
+                   help="op order in the passes: reorder (library default: commuting ops scheduled into fewer "
+                        "passes, within 1e-12 of the reference) or exact (circuit order, bit-identical)")
+    p.add_argument("--no-exact-side", action="store_true",
+                   help="skip the circuit-order side measurement of a reorder run")
     p.add_argument("--transport", choices=["peer", "nccl"], default="peer", help="N > 1 data plane")
     p.add_argument("--swaps", type=int, default=1, help="N > 1: global<->local qubit swaps (0: exchange per gate)")
     a = p.parse_args()
@@ -325,6 +330,7 @@ def run_ours(args):
         env.set_qubit_swaps(bool(args.swaps))
     else:
         env = quest.Env()
+    env.set_ordering(args.order == "reorder")
     if args.fusion or args.reg_qubits:
         env.set_fusion(args.fusion, 0, args.reg_qubits)
     if args.jit is not None:
@@ -430,6 +436,38 @@ def run_ours(args):
             single = {"gates": int(p1.size), "avg_pass_ms": round(float(p1.mean()), 4),
                       "achieved_GBps": round(gbs, 1), "frac": round(gbs / pk["hbm_gbs"], 4),
                       "what": "one gate per tile pass (fusion mode 1), same kernel, same bytes per pass"}
+
+    # side measurement: the same circuit in circuit order (bit-identical to
+    # the reference), same register, same timing
+    exact = None
+    if args.order == "reorder" and not args.no_exact_side and args.fusion == 0:
+        env.set_ordering(False)
+        for _ in range(max(2, args.warmup)):
+            C.apply_circuit(q, circuit)
+            q.flush()
+            env.sync()
+            quest.jit_wait()
+        barrier()
+        p0x = q.pass_count()
+        env.profile_start()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            C.apply_circuit(q, circuit)
+            q.flush()
+        e1.record(stream)
+        barrier()
+        ms_x, k_x = env.profile_stop()
+        t_x = allmax(e0.elapsed_time(e1))
+        p_x = ms_x[k_x == 0]
+        exact = {"order": "circuit order (bit-identical to the reference)",
+                 "value": round(effective_bytes(n, gates * args.steps) / (t_x / 1e3) / 1e9, 1), "unit": UNIT,
+                 "ms_per_step": round(t_x / args.steps, 3), "ms_per_gate": round(t_x / (gates * args.steps), 4),
+                 "passes_per_step": (q.pass_count() - p0x) / args.steps,
+                 "avg_pass_ms": round(float(p_x.mean()), 4) if p_x.size else None,
+                 "pass_roofline_frac": round(per_launch_bytes / (float(p_x.mean()) / 1e3) / 1e9 / pk["hbm_gbs"], 4)
+                 if p_x.size else None}
+        env.set_ordering(True)
 
     # side measurement: the same circuit on a single-precision register
     sp = None
@@ -542,6 +580,9 @@ def run_ours(args):
                                       + (f", {args.transport} transport, qubit swaps {'on' if args.swaps else 'off'}"
                                          if world > 1 else ""),
                        "precision": args.precision,
+                       "order": ("reorder: commuting ops scheduled into fewer passes (amplitudes within 1e-12 "
+                                 "of the reference, tests/test_gpu_reorder.py)" if args.order == "reorder"
+                                 else "exact: circuit order (bit-identical to the reference)"),
                        "l2": f"state {AMP << args.local_qubits >> 30} GiB per GPU >> 126 MB L2 (no flush needed)",
                        "passes_per_step": passes / args.steps, "fusion": args.fusion,
                        "jit": {"mode": quest.lib().qgpuGetJit(), "kernels": quest.jit_stats()[0],
@@ -568,6 +609,7 @@ def run_ours(args):
                          "per_pass_bound": bound, "passes_by_op_count": classes},
             "clocks": clocks.summary(),
             "check": {"norm_error_after_timed_steps": norm_error},
+            "circuit_order": exact,
             "single_gate_pass": single,
             "single_precision": sp,
             "c5": c5,

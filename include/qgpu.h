@@ -149,6 +149,29 @@ void qgpuSetExchangeChunk(QuESTEnv env, long long int amps);
  * first returned to the identity qubit layout. */
 void qgpuSetQubitSwaps(QuESTEnv env, int enable);
 
+/* Op order inside the fused HBM passes. 1 (default): ops that commute (they
+ * meet only on qubits both act on diagonally — controls, phases, dephasing,
+ * collapse — or share no qubit) are scheduled out of circuit order into
+ * fewer passes; amplitudes equal the reference's up to rounding (within
+ * 1e-12 max-abs, tested at 30 qubits), not bit for bit. 0: circuit order,
+ * bit-identical to the reference (kernels.cpp:105-112, fma chain included).
+ * windowOps > 0 sets how many queued ops the scheduler looks ahead (default
+ * 512). Queued ops of this env's registers are flushed first. Environment:
+ * QGPU_ORDER=exact|reorder, QGPU_WINDOW=n. */
+void qgpuSetOrdering(QuESTEnv env, int reorder, int windowOps);
+int qgpuGetOrdering(QuESTEnv env);
+
+/* The tile-pass scheduler alone (host only, no GPU): numOps physical ops on
+ * a flatQubits-qubit local state (kinds: 0 gate with its 8-double matrix
+ * (re, im row-major) in mats[8 i], 1 dephasing, 2 depolarising on (q0, q1),
+ * 3 collapse), scheduled as a register of that size would with the given
+ * ordering, window and phase limit. Writes, per executed op in execution
+ * order, its input index, pass and phase; returns the number of passes, or
+ * -1 on invalid input. */
+int qgpuPlanPasses(int flatQubits, int numOps, const int* kinds, const int* q0, const int* q1,
+                   const unsigned long long* cmasks, const double* mats, int reorder, int windowOps,
+                   int maxPhases, int* orderOut, int* passOut, int* phaseOut);
+
 /* The swap planner alone (host only, no GPU): for numOps ops on logical
  * flat qubits targets[k] (pairOps[k] != 0 for a 2x2 non-diagonal gate,
  * 0 for a diagonal op) on 2^rankLog2 ranks, the swaps the runtime performs:

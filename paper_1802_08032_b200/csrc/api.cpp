@@ -330,6 +330,12 @@ QuESTEnv make_env(Mode mode, int rank, int nranks, int device, const char* id128
     e->rng = fold_seeds(seeds, 2);
     if (const char* v = std::getenv("QGPU_TILE_TARGETS"))
         e->tile_targets = std::clamp(std::atoi(v), 1, qgpu::kTileHigh);
+    if (const char* v = std::getenv("QGPU_ORDER")) {
+        if (!std::strcmp(v, "exact") || !std::strcmp(v, "0")) e->order = 0;
+        else if (!std::strcmp(v, "reorder") || !std::strcmp(v, "1")) e->order = 1;
+        else throw qgpu::DomainError(std::string("QGPU_ORDER must be exact or reorder, got ") + v);
+    }
+    if (const char* v = std::getenv("QGPU_WINDOW")) e->window = std::clamp(std::atoi(v), 1, 65536);
     if (const char* v = std::getenv("QGPU_TILE_PHASES"))
         e->tile_phases = std::clamp(std::atoi(v), 1, qgpu::kMaxPhases);
     if (mode == Mode::Nccl && nranks > 1) e->nccl = std::make_unique<NcclComm>(rank, nranks, id128);
@@ -580,7 +586,10 @@ void qgpuSetFusion(QuESTEnv env, int mode, int maxOps, int regQubits) {
                                     " register qubits");
         for (QuregImpl* q : e->quregs) q->flush();
         e->fusion_mode = mode;
-        if (maxOps > 0) e->max_ops = maxOps;
+        if (maxOps > 0) {
+            e->max_ops = maxOps;
+            e->tile_max_ops = maxOps;
+        }
         if (regQubits > 0) e->reg_qubits = regQubits;
     });
 }
@@ -1261,6 +1270,79 @@ int qgpuDeviceMaxQubits(unsigned long long deviceBytes, int rankLog2, unsigned l
     return guarded("qgpuDeviceMaxQubits", -1, [&] {
         return qgpu::device_max_qubits(deviceBytes, rankLog2, chunkAmps, density != 0, singlePrecision != 0);
     });
+}
+
+int qgpuPlanPasses(int flatQubits, int numOps, const int* kinds, const int* q0, const int* q1,
+                   const unsigned long long* cmasks, const double* mats, int reorder, int windowOps,
+                   int maxPhases, int* orderOut, int* passOut, int* phaseOut) {
+    return guarded("qgpuPlanPasses", -1, [&] {
+        if (flatQubits < kTileQubits || flatQubits > 62 || numOps < 0 || maxPhases < 1 || maxPhases > kMaxPhases)
+            throw qgpu::DomainError("invalid pass-plan request");
+        Env e;
+        e.order = reorder ? 1 : 0;
+        if (windowOps > 0) e.window = windowOps;
+        e.tile_phases = maxPhases;
+        QuregImpl q;
+        q.N = q.flat = flatQubits;
+        q.local_qubits = flatQubits;
+        q.local_len = uint64_t{1} << flatQubits;
+        std::vector<QuregImpl::PlannedPass> out;
+        q.plan_sink = &out;
+        q.env = &e;
+        try {
+            for (int i = 0; i < numOps; ++i) {
+                FlatOp op;
+                op.kind = static_cast<uint8_t>(kinds[i]);
+                op.q0 = q0[i];
+                op.q1 = q1[i];
+                op.cmask = cmasks[i];
+                op.id = i;
+                if (op.q0 < 0 || op.q0 >= flatQubits || op.q1 >= flatQubits || (op.cmask >> flatQubits))
+                    throw qgpu::DomainError("op " + std::to_string(i) + " out of range");
+                if (op.kind == FK_GATE) {
+                    std::memcpy(op.m, mats + 8 * static_cast<size_t>(i), sizeof(op.m));
+                    op.cls = classify(op.m, &op.flags);
+                } else if (op.kind > FK_COLLAPSE) {
+                    throw qgpu::DomainError("op " + std::to_string(i) + ": unknown kind");
+                }
+                q.enqueue_phys(op);
+            }
+            q.flush_pass();
+        } catch (...) {
+            q.env = nullptr;
+            throw;
+        }
+        q.env = nullptr;
+        int k = 0;
+        for (size_t p = 0; p < out.size(); ++p) {
+            const auto& pp = out[p];
+            for (size_t j = 0; j < pp.ids.size(); ++j, ++k) {
+                int ph = 0;
+                while (ph + 1 < static_cast<int>(pp.phase_begin.size()) && pp.phase_begin[ph + 1] <= static_cast<int>(j)) ++ph;
+                if (k >= numOps) throw qgpu::DeviceError("internal: plan has more ops than the input");
+                orderOut[k] = pp.ids[j];
+                passOut[k] = static_cast<int>(p);
+                phaseOut[k] = ph;
+            }
+        }
+        if (k != numOps) throw qgpu::DeviceError("internal: plan lost ops");
+        return static_cast<int>(out.size());
+    });
+}
+
+void qgpuSetOrdering(QuESTEnv env, int reorder, int windowOps) {
+    guarded_void("qgpuSetOrdering", [&] {
+        Env* e = env_of(env);
+        if (reorder != 0 && reorder != 1) throw qgpu::DomainError("ordering must be 0 (circuit order) or 1 (reorder)");
+        if (windowOps < 0 || windowOps > 65536) throw qgpu::DomainError("reorder window must be 0..65536 ops");
+        for (QuregImpl* q : e->quregs) q->flush();
+        e->order = reorder;
+        if (windowOps > 0) e->window = windowOps;
+    });
+}
+
+int qgpuGetOrdering(QuESTEnv env) {
+    return guarded("qgpuGetOrdering", -1, [&] { return env_of(env)->order; });
 }
 
 void qgpuSetQubitSwaps(QuESTEnv env, int enable) {

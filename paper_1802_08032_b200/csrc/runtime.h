@@ -51,7 +51,8 @@ struct Env {
     int rank_log2 = 0;
     uint64_t rng = 0;    // SplitMix64 state for measure()
     int fusion_mode = 0; // 0 fused, 1 one pass per op, 2 simple per-op kernels
-    int max_ops = kMaxPassOps;
+    int max_ops = kMaxPassOps;      // register-only passes (small states)
+    int tile_max_ops = kMaxTileOps; // tile passes (qgpuSetFusion's maxOps sets both)
     int reg_qubits = 4;
     // tile-pass shape limits (scheduler tuning; QGPU_TILE_TARGETS /
     // QGPU_TILE_PHASES override them at Env creation). A phase transition
@@ -66,6 +67,12 @@ struct Env {
     // global<->local qubit swaps instead of per-gate exchanges (swap_plan.h);
     // qgpuSetQubitSwaps turns them off (the reference's exchange per gate)
     bool qubit_swaps = true;
+    // op order inside the tile passes (qgpuSetOrdering / QGPU_ORDER):
+    // 1 (default) schedules commuting ops out of circuit order into fewer
+    // passes (amplitudes within 1e-12 of the reference, not bit-identical);
+    // 0 keeps circuit order (bit-identical to the reference)
+    int order = 1;
+    int window = 512; // ops the reorder scheduler looks ahead (QGPU_WINDOW)
     std::unique_ptr<NcclComm> nccl;
     std::unique_ptr<PeerGroup> peer;
     bool multi_process() const { return mode == Mode::Nccl || mode == Mode::Peer; }
@@ -119,6 +126,7 @@ struct FlatOp {
     int q0 = 0, q1 = -1;
     uint64_t cmask = 0;
     double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    int32_t id = -1; // caller's op index (qgpuPlanPasses dry runs)
 };
 
 uint8_t classify(const double* m, uint8_t* diag_flags);
@@ -163,6 +171,21 @@ struct QuregImpl {
     std::vector<int> tile_high;      // tile pass: high qubits in the tile
     std::vector<PhaseState> phases;  // tile pass: phases
 
+    // Reorder window (Env::order == 1, tile passes): physical ops awaiting
+    // pass formation. A pass is cut from the window by commutation, not by
+    // position (window_pass); pending / phases then hold that pass only.
+    std::vector<FlatOp> win;
+    bool reorder_on() const;
+    void window_pass();  // form and launch one pass from the window
+    void window_drain(); // ... until the window is empty
+
+    // Dry run (qgpuPlanPasses): passes are recorded here instead of launched
+    struct PlannedPass {
+        std::vector<int> ids;         // FlatOp::id in execution order
+        std::vector<int> phase_begin; // index into ids where each phase starts
+    };
+    std::vector<PlannedPass>* plan_sink = nullptr;
+
     // logical -> physical qubit map (global<->local swaps, swap_plan.h)
     SwapPlanner sp;
 
@@ -182,6 +205,7 @@ struct QuregImpl {
     void flush();
     void discard_all() { // queued ops are dead (the state is overwritten)
         lq.clear();
+        win.clear();
         deferred.clear();
         ++version;
         discard();

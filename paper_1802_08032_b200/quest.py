@@ -160,6 +160,9 @@ _SIGS = {
     "qgpuTrace": (Complex, [Qureg]),
     "qgpuSetExchangeChunk": (None, [QuESTEnv, _LL]),
     "qgpuSetQubitSwaps": (None, [QuESTEnv, _I]),
+    "qgpuSetOrdering": (None, [QuESTEnv, _I, _I]),
+    "qgpuGetOrdering": (_I, [QuESTEnv]),
+    "qgpuPlanPasses": (_I, [_I, _I, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _VP, _VP, _VP]),
     "qgpuPlanSwaps": (_I, [_I, _I, _ULL, _I, _VP, _VP, _VP, _I]),
     "qgpuCommStats": (None, [Qureg, _VP, _VP]),
     "qgpuPlanGate": (_I, [_I, _I, _I, _I, _ULL, _IP, _IP, ctypes.POINTER(ctypes.c_ulonglong)]),
@@ -305,6 +308,15 @@ class Env:
         """Global<->local qubit swaps (True, default) or the reference's
         exchange per global-target gate (False)."""
         call("qgpuSetQubitSwaps", self.h, int(enable))
+
+    def set_ordering(self, reorder: bool, window: int = 0):
+        """Commutation-aware pass scheduling (True, default: within 1e-12 of
+        the reference) or circuit order (False: bit-identical)."""
+        call("qgpuSetOrdering", self.h, int(reorder), int(window))
+
+    @property
+    def reorder(self) -> bool:
+        return bool(call("qgpuGetOrdering", self.h))
 
     @property
     def stream(self) -> int:
@@ -498,6 +510,34 @@ def plan_swaps(flat: int, rank_log2: int, ops, chunk_amps: int = 1 << 24):
     if n < 0:
         check()
     return [tuple(int(x) for x in out[3 * i:3 * i + 3]) for i in range(n)]
+
+
+def plan_passes(flat: int, ops, reorder: bool = True, window: int = 0, max_phases: int = 3):
+    """qgpuPlanPasses (host only): ops = [(kind, q0, q1, cmask, m8)], kind 0
+    gate (m8: a, b, c, d as interleaved re / im), 1 dephasing, 2
+    depolarising, 3 collapse. Returns (order, pass, phase) arrays over the
+    executed ops: the input index, pass and phase of each, in execution
+    order."""
+    import numpy as np
+
+    n = len(ops)
+    kinds = np.array([o[0] for o in ops], dtype=np.int32)
+    q0 = np.array([o[1] for o in ops], dtype=np.int32)
+    q1 = np.array([o[2] for o in ops], dtype=np.int32)
+    cm = np.array([o[3] for o in ops], dtype=np.uint64)
+    mats = np.zeros((max(1, n), 8), dtype=np.float64)
+    for i, o in enumerate(ops):
+        if o[0] == 0:
+            mats[i] = o[4]
+    order = np.zeros(max(1, n), dtype=np.int32)
+    pas = np.zeros(max(1, n), dtype=np.int32)
+    phase = np.zeros(max(1, n), dtype=np.int32)
+    r = lib().qgpuPlanPasses(flat, n, kinds.ctypes.data, q0.ctypes.data, q1.ctypes.data, cm.ctypes.data,
+                             mats.ctypes.data, int(reorder), window, max_phases, order.ctypes.data,
+                             pas.ctypes.data, phase.ctypes.data)
+    if r < 0:
+        check()
+    return order[:n], pas[:n], phase[:n]
 
 
 def set_jit(mode: int):
