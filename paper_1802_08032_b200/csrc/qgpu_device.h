@@ -169,6 +169,7 @@ enum TileCode : uint8_t {
     TC_COLLAPSE = 50,
     TC_DEPOL = 51, // + register-bit pair (0,1) (0,2) (0,3) (1,2) (1,3) (2,3): 51..56
     TC_DEPOL_LANE = 57, // + register bit of t+N, t on a lane bit: 57..60
+    TC_LANE_RX = 61,    // Rx-class 2x2 on a lane bit (tolerance mode only: TileParams.fast)
 };
 
 // Op header packed in one 64-bit word (one constant-bank load per op):
@@ -228,6 +229,9 @@ struct TileParams {
     int32_t high_sorted[kTileHigh];        // the same qubits, ascending
     int32_t any_outer;                     // some op has controls outside the tile
     int32_t single;                        // amplitudes are float2 (else double2)
+    // tolerance-mode handlers (the reordering schedule, Env::order == 1):
+    // lane ops without operand selects, Rx-class lane ops
+    int32_t fast;
     uint64_t seg_off[1 << kTileHigh];      // global offset of tile segment s
     // the last phase stores straight to HBM: local-index offsets of its
     // register i, warp w and lane bits 3, 4 (lane bits 0-2: qubits 0-2)

@@ -756,7 +756,7 @@ int pass_profile_info(const TileParams& P) {
             f = (code - TC_REG_SEL) / 4 == 0 ? 8.0 : 0.0;
         } else if (code == TC_LANE_GENERIC || code == TC_LANE_SEL_GENERIC) {
             f = 8.0;
-        } else if (code == TC_LANE_REAL) {
+        } else if (code == TC_LANE_REAL || code == TC_LANE_RX) {
             f = 4.0;
         } else if (code == TC_LANE_SWAP || code == TC_LANE_SEL_SWAP) {
             f = 0.0;
@@ -817,6 +817,7 @@ void QuregImpl::launch_tile() {
     std::memset(&P, 0, sizeof(P));
     P.num_tiles = uint64_t{1} << (local_qubits - kTileQubits);
     P.single = single ? 1 : 0;
+    P.fast = env->order == 1 ? 1 : 0; // tolerance-mode handlers with the reordering schedule
     P.num_phases = static_cast<int>(phases.size());
     for (int j = 0; j < kTileHigh; ++j) P.high_pos[j] = high[j];
     for (int s = 0; s < (1 << kTileHigh); ++s) {
@@ -1136,9 +1137,10 @@ void QuregImpl::launch_tile() {
                 }
             } else if (q0k == TL_LANE) {
                 if (!ctrl)
-                    code = op.cls == CLS_SWAP   ? TC_LANE_SWAP
-                           : op.cls == CLS_REAL ? TC_LANE_REAL
-                                                : TC_LANE_GENERIC;
+                    code = op.cls == CLS_SWAP                    ? TC_LANE_SWAP
+                           : op.cls == CLS_REAL                  ? TC_LANE_REAL
+                           : op.cls == CLS_RX && P.fast ? TC_LANE_RX
+                                                                 : TC_LANE_GENERIC;
                 else
                     code = op.cls == CLS_SWAP ? TC_LANE_SEL_SWAP : TC_LANE_SEL_GENERIC;
             } else { // register bit

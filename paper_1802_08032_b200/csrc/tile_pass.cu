@@ -14,16 +14,16 @@ namespace qgpu {
 
 namespace {
 
-template <int RB, int WB, int NBUF>
+template <int RB, int WB, int NBUF, bool FAST>
 __global__ void __launch_bounds__(kTileThreads, 1)
 k_tile_pass(double2* __restrict__ amps, const __grid_constant__ TileParams P) {
-    tile_f64::tile_pass_body<RB, WB, NBUF, tile_f64::Interp>(amps, P);
+    tile_f64::tile_pass_body<RB, WB, NBUF, tile_f64::Interp<FAST>>(amps, P);
 }
 
-template <int RB, int WB, int NBUF>
+template <int RB, int WB, int NBUF, bool FAST>
 __global__ void __launch_bounds__(kTileThreads, kTileCtasF32)
 k_tile_pass_f32(float2* __restrict__ amps, const __grid_constant__ TileParams P) {
-    tile_f32::tile_pass_body<RB, WB, NBUF, tile_f32::Interp>(amps, P);
+    tile_f32::tile_pass_body<RB, WB, NBUF, tile_f32::Interp<FAST>>(amps, P);
 }
 
 } // namespace
@@ -63,13 +63,15 @@ void launch_tile_pass(void* amps, const TileParams& p, cudaStream_t s) {
     }
     constexpr int NBUF = kTileStages;
     if (p.single) {
-        static bool set = false;
-        launch_interp(k_tile_pass_f32<kPhaseRegBits, kTileWarpBits, NBUF>, amps, p, s,
-                      NBUF * (sizeof(float2) << kTileQubits), set, kTileCtasF32);
+        static bool set[2] = {false, false};
+        launch_interp(p.fast ? k_tile_pass_f32<kPhaseRegBits, kTileWarpBits, NBUF, true>
+                             : k_tile_pass_f32<kPhaseRegBits, kTileWarpBits, NBUF, false>,
+                      amps, p, s, NBUF * (sizeof(float2) << kTileQubits), set[p.fast ? 1 : 0], kTileCtasF32);
     } else {
-        static bool set = false;
-        launch_interp(k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF>, amps, p, s,
-                      NBUF * (sizeof(double2) << kTileQubits), set, kTileCtasF64);
+        static bool set[2] = {false, false};
+        launch_interp(p.fast ? k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF, true>
+                             : k_tile_pass<kPhaseRegBits, kTileWarpBits, NBUF, false>,
+                      amps, p, s, NBUF * (sizeof(double2) << kTileQubits), set[p.fast ? 1 : 0], kTileCtasF64);
     }
     count_launch();
 }
