@@ -336,6 +336,9 @@ QuESTEnv make_env(Mode mode, int rank, int nranks, int device, const char* id128
         else throw qgpu::DomainError(std::string("QGPU_ORDER must be exact or reorder, got ") + v);
     }
     if (const char* v = std::getenv("QGPU_WINDOW")) e->window = std::clamp(std::atoi(v), 1, 65536);
+    if (const char* v = std::getenv("QGPU_LANE_CAP")) e->lane_cap = std::max(0, std::atoi(v));
+    if (const char* v = std::getenv("QGPU_INTERLEAVE")) e->interleave = std::atoi(v) != 0;
+    if (const char* v = std::getenv("QGPU_NORMALIZE")) e->normalize = std::atoi(v) != 0;
     if (const char* v = std::getenv("QGPU_TILE_PHASES"))
         e->tile_phases = std::clamp(std::atoi(v), 1, qgpu::kMaxPhases);
     if (mode == Mode::Nccl && nranks > 1) e->nccl = std::make_unique<NcclComm>(rank, nranks, id128);
@@ -1279,6 +1282,8 @@ int qgpuPlanPasses(int flatQubits, int numOps, const int* kinds, const int* q0, 
         if (flatQubits < kTileQubits || flatQubits > 62 || numOps < 0 || maxPhases < 1 || maxPhases > kMaxPhases)
             throw qgpu::DomainError("invalid pass-plan request");
         Env e;
+        if (const char* v = std::getenv("QGPU_LANE_CAP")) e.lane_cap = std::max(0, std::atoi(v));
+        if (const char* v = std::getenv("QGPU_INTERLEAVE")) e.interleave = std::atoi(v) != 0;
         e.order = reorder ? 1 : 0;
         if (windowOps > 0) e.window = windowOps;
         e.tile_phases = maxPhases;
@@ -1316,13 +1321,15 @@ int qgpuPlanPasses(int flatQubits, int numOps, const int* kinds, const int* q0, 
         int k = 0;
         for (size_t p = 0; p < out.size(); ++p) {
             const auto& pp = out[p];
-            for (size_t j = 0; j < pp.ids.size(); ++j, ++k) {
+            for (size_t j = 0; j < pp.ids.size(); ++j) {
+                if (pp.ids[j] < 0) continue; // the scheduler's own ops (a folded-out scalar)
                 int ph = 0;
                 while (ph + 1 < static_cast<int>(pp.phase_begin.size()) && pp.phase_begin[ph + 1] <= static_cast<int>(j)) ++ph;
                 if (k >= numOps) throw qgpu::DeviceError("internal: plan has more ops than the input");
                 orderOut[k] = pp.ids[j];
                 passOut[k] = static_cast<int>(p);
                 phaseOut[k] = ph;
+                ++k;
             }
         }
         if (k != numOps) throw qgpu::DeviceError("internal: plan lost ops");

@@ -408,8 +408,146 @@ inline bool blocked_by(const OpQubits& a, uint64_t bnd, uint64_t bdg) {
 }
 } // namespace
 
+// Unit-coefficient normalization (tolerance mode): an uncontrolled real or
+// Rx-class gate is its largest-magnitude coefficient v times a matrix whose
+// entries include exact +-1 (H -> [[1, 1], [1, -1]] and 1/sqrt 2; Ry(t) ->
+// [[1, -tan], [tan, 1]] and cos, or [[cot, -1], [1, cot]] and -sin; Rx
+// alike with i), and an uncontrolled diagonal is a times diag(1, d / a) (Rz
+// -> diag(1, e^{i theta}) and e^{-i theta / 2}). The kernels skip the
+// multiplications by +-1 (tile header unit bits) and the identity half of a
+// diagonal: roughly half the FP64 work of the layered circuit. The scalars
+// commute with every linear op, so they are multiplied together and applied
+// once, folded into one op of some pass (fold_scale) — before the window
+// drains empty, i.e. before anything reads the state.
+bool QuregImpl::normalize_op(FlatOp& op) {
+    if (op.kind != FK_GATE || op.cmask != 0) return false;
+    double* m = op.m;
+    double vr, vi;
+    if (op.cls == CLS_DIAG) {
+        if (op.flags & DF_A_ONE) return false;
+        const double ar = m[0], ai = m[1], den = ar * ar + ai * ai;
+        if (!(den > 0.0)) return false;
+        const double dr = (m[6] * ar + m[7] * ai) / den, di = (m[7] * ar - m[6] * ai) / den;
+        vr = ar;
+        vi = ai;
+        m[0] = 1.0;
+        m[1] = 0.0;
+        m[6] = dr;
+        m[7] = di;
+        op.flags = DF_A_ONE | ((dr == 1.0 && di == 0.0) ? DF_D_ONE : 0);
+    } else if (op.cls == CLS_REAL || op.cls == CLS_RX) {
+        static const int kReal[4] = {0, 2, 4, 6}, kRx[4] = {0, 3, 5, 6};
+        const int* idx = op.cls == CLS_REAL ? kReal : kRx;
+        double v = m[idx[0]];
+        for (int k = 1; k < 4; ++k)
+            if (std::fabs(m[idx[k]]) > std::fabs(v)) v = m[idx[k]];
+        if (!(std::fabs(v) > 0.0) || !std::isfinite(v)) return false;
+        uint8_t unit = 0;
+        for (int k = 0; k < 4; ++k) {
+            m[idx[k]] /= v;
+            if (m[idx[k]] == 1.0) unit |= static_cast<uint8_t>(1u << (2 * k));
+            if (m[idx[k]] == -1.0) unit |= static_cast<uint8_t>(2u << (2 * k));
+        }
+        op.unit = unit;
+        vr = v;
+        vi = 0.0;
+    } else {
+        return false;
+    }
+    const double r = gscale_re * vr - gscale_im * vi, i = gscale_re * vi + gscale_im * vr;
+    gscale_re = r;
+    gscale_im = i;
+    return true;
+}
+
+// Applies the pending scalar to one uncontrolled gate of the open pass,
+// the cheapest available: a generic 2x2 (free), a diagonal (its identity
+// half comes back), a real / Rx-class gate (loses its unit entries; becomes
+// generic if the scalar is complex). Returns false if the pass has none.
+bool QuregImpl::fold_scale() {
+    if (gscale_re == 1.0 && gscale_im == 0.0) return true;
+    int best = -1, best_cost = 1 << 30;
+    for (size_t k = 0; k < pending.size(); ++k) {
+        const FlatOp& op = pending[k];
+        if (op.kind != FK_GATE || op.cmask != 0) continue;
+        int cost;
+        if (op.cls == CLS_GENERIC) cost = 0;
+        else if (op.cls == CLS_DIAG) cost = 2;
+        else if (op.cls == CLS_REAL || op.cls == CLS_RX) cost = gscale_im == 0.0 ? 2 : 6;
+        else continue; // swaps stay pure moves
+        if (cost < best_cost) {
+            best_cost = cost;
+            best = static_cast<int>(k);
+        }
+    }
+    if (best < 0) return false;
+    FlatOp& op = pending[best];
+    const double sr = gscale_re, si = gscale_im;
+    if (op.cls == CLS_REAL || op.cls == CLS_RX) {
+        // expand the unit entries back to their values (they were exact)
+        op.unit = 0;
+        if (si != 0.0) op.cls = CLS_GENERIC;
+    }
+    for (int k = 0; k < 8; k += 2) {
+        const double a = op.m[k], b = op.m[k + 1];
+        op.m[k] = a * sr - b * si;
+        op.m[k + 1] = a * si + b * sr;
+    }
+    if (op.cls == CLS_DIAG) {
+        op.flags = 0;
+        if (op.m[0] == 1.0 && op.m[1] == 0.0) op.flags |= DF_A_ONE;
+        if (op.m[6] == 1.0 && op.m[7] == 0.0) op.flags |= DF_D_ONE;
+    }
+    gscale_re = 1.0;
+    gscale_im = 0.0;
+    return true;
+}
+
 bool QuregImpl::reorder_on() const {
     return env->order == 1 && use_tile() && env->fusion_mode == 0;
+}
+
+// Reorders pending[begin, end) — one phase — so that shuffle-bound lane ops
+// alternate with the other ops where dependencies allow (list scheduling,
+// earliest ready op of the wanted kind first): the compiler then overlaps a
+// lane op's shuffles with its neighbours' FP64 work in the straight-line
+// JIT program instead of running a burst of lane ops shuffle-bound.
+void QuregImpl::interleave_lane_ops(int begin, const std::vector<int>& R) {
+    const int n = static_cast<int>(pending.size()) - begin;
+    if (n < 3) return;
+    const int lf = lane_fixed();
+    std::vector<OpQubits> oq(n);
+    std::vector<char> lane(n), done(n, 0);
+    int nl = 0;
+    for (int i = 0; i < n; ++i) {
+        const FlatOp& op = pending[begin + i];
+        oq[i] = op_qubits(op);
+        lane[i] = op.kind == FK_GATE && op.cls != CLS_DIAG && op.q0 < kLaneQubits &&
+                  (op.q0 < lf || std::find(R.begin(), R.end(), op.q0) == R.end());
+        nl += lane[i];
+    }
+    if (nl == 0 || nl == n) return;
+    std::vector<FlatOp> out;
+    out.reserve(n);
+    bool want_lane = false;
+    for (int k = 0; k < n; ++k) {
+        int pick = -1, any = -1;
+        uint64_t bnd = 0, bdg = 0;
+        for (int i = 0; i < n; ++i) {
+            if (done[i]) continue;
+            if (!blocked_by(oq[i], bnd, bdg)) {
+                if (any < 0) any = i;
+                if (pick < 0 && lane[i] == want_lane) pick = i;
+            }
+            bnd |= oq[i].nd;
+            bdg |= oq[i].dg;
+        }
+        if (pick < 0) pick = any;
+        done[pick] = 1;
+        out.push_back(pending[begin + pick]);
+        want_lane = !lane[pick];
+    }
+    std::copy(out.begin(), out.end(), pending.begin() + begin);
 }
 
 void QuregImpl::window_drain() {
@@ -482,6 +620,20 @@ void QuregImpl::window_pass() {
         }
         return k;
     };
+    // Lane ops (pair targets on lane bits: 4 warp shuffles per amplitude)
+    // are taken eagerly by the tile choice (lanes are always in the tile), so
+    // without a cap they pile up in the first passes, where the shuffle unit
+    // (1 warp instruction / clock / SM) rather than the FP64 pipe bounds the
+    // pass; capped per pass they spread out and overlap the FP64 work of the
+    // register ops (Env::lane_cap, QGPU_LANE_CAP; 0 = no cap).
+    int lane_ops = 0;
+    auto shuffles = [&](size_t j, const std::vector<int>& R) {
+        const FlatOp& op = win[j];
+        if (op.kind == FK_DEPOL) return op.q0 < lf;
+        if (op.kind != FK_GATE || op.cls == CLS_DIAG || op.q0 >= kLaneQubits) return false;
+        if (op.q0 < lf) return true;
+        return !in(R, op.q0) && static_cast<int>(R.size()) >= kPhaseRegBits; // 3, 4 as lane bits
+    };
     while (static_cast<int>(phases.size()) < maxph && pending.size() < cap) {
         PhaseState ph;
         ph.op_begin = static_cast<int>(pending.size());
@@ -495,8 +647,11 @@ void QuregImpl::window_pass() {
                 for (size_t j = 0; j < W; ++j) {
                     if (!sel[j] || taken[j]) continue;
                     int qs[2];
-                    if (pending.size() < cap && !blocked_by(oq[j], bnd, bdg) && missing(j, R, qs) == 0) {
+                    const bool lane = shuffles(j, R);
+                    if (pending.size() < cap && !blocked_by(oq[j], bnd, bdg) && missing(j, R, qs) == 0 &&
+                        !(lane && env->lane_cap > 0 && lane_ops >= env->lane_cap)) {
                         const FlatOp& op = win[j];
+                        if (lane) ++lane_ops;
                         // qubits 3, 4: a register qubit while the phase has
                         // room, else a lane op (as place_tile)
                         if (op.kind == FK_GATE && op.cls != CLS_DIAG && op.q0 >= lf && op.q0 < kLaneQubits &&
@@ -534,6 +689,7 @@ void QuregImpl::window_pass() {
             R.push_back(bq);
         }
         if (!any) break;
+        if (env->interleave) interleave_lane_ops(ph.op_begin, R);
         phases.push_back(ph);
     }
     if (pending.empty()) throw DeviceError("internal: reorder scheduler formed an empty pass");
@@ -546,6 +702,25 @@ void QuregImpl::window_pass() {
     for (size_t j = 0; j < W; ++j)
         if (!taken[j]) win[k++] = win[j];
     win.resize(k);
+    if (!fold_scale() && win.empty()) {
+        // the window drains with the scalar unapplied: one elementwise op
+        // (any qubit; qubit 0: a lane diagonal) in this pass, or the next
+        FlatOp sc;
+        sc.kind = FK_GATE;
+        sc.cls = CLS_DIAG;
+        sc.q0 = 0;
+        sc.m[0] = sc.m[6] = gscale_re;
+        sc.m[1] = sc.m[7] = gscale_im;
+        if (pending.size() < cap) {
+            pending.push_back(sc);
+            gscale_re = 1.0;
+            gscale_im = 0.0;
+        } else {
+            win.push_back(sc); // carries its own scalar: the pending one is in it
+            gscale_re = 1.0;
+            gscale_im = 0.0;
+        }
+    }
     launch_tile();
     discard();
 }
@@ -613,6 +788,7 @@ void QuregImpl::enqueue_phys(const FlatOp& op) {
                                   : !(pair && op.q0 >= local_qubits);
         if (tileable) {
             win.push_back(op);
+            if (env->normalize) normalize_op(win.back());
             if (static_cast<int>(win.size()) >= env->window) window_pass();
             return;
         }
@@ -749,15 +925,20 @@ int pass_profile_info(const TileParams& P) {
         const int code = static_cast<int>(h & 63);
         const uint32_t flags = (h >> 6) & 15u;
         double f;
+        const uint32_t un = static_cast<uint32_t>((h >> 40) & 0xff);
+        auto u = [&](int k) { return (un >> (2 * k)) & 3u; };
         if (code < TC_REG + 16) { // 2x2 on a register bit, by class row
             const int row = (code - TC_REG) / 4;
             f = row == 0 ? 8.0 : row == 3 ? 0.0 : 4.0;
+            if (row == 1 || row == 2) // unit coefficients: one FMA (or add) per component
+                f = ((u(0) || u(1)) ? 1.0 : 2.0) + ((u(2) || u(3)) ? 1.0 : 2.0);
         } else if (code < TC_REG_SEL + 8) {
             f = (code - TC_REG_SEL) / 4 == 0 ? 8.0 : 0.0;
         } else if (code == TC_LANE_GENERIC || code == TC_LANE_SEL_GENERIC) {
             f = 8.0;
         } else if (code == TC_LANE_REAL || code == TC_LANE_RX) {
-            f = 4.0;
+            const bool uni = (u(1) && u(1) == u(2)) || (u(0) && u(0) == u(3));
+            f = uni ? 2.0 : 4.0;
         } else if (code == TC_LANE_SWAP || code == TC_LANE_SEL_SWAP) {
             f = 0.0;
         } else if ((code >= TC_DIAG_REG_D && code < TC_DIAG_REG_D + 4) ||
@@ -1152,6 +1333,7 @@ void QuregImpl::launch_tile() {
                 }
             }
             to.hdr = tile_hdr(code, flags, op.outcome, q0k, q0p, q1k, q1p, lane_cm, reg_cm, warp_cm);
+            if (P.fast) to.hdr |= static_cast<uint64_t>(op.unit) << 40; // unit coefficients
             // a diagonal gate with a == 1 exactly (Z, S, T, phase shifts)
             // on a qubit outside the tile is the identity wherever that bit
             // is 0: a control on it, so those tiles skip the op

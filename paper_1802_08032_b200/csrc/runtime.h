@@ -73,6 +73,10 @@ struct Env {
     // 0 keeps circuit order (bit-identical to the reference)
     int order = 1;
     int window = 512; // ops the reorder scheduler looks ahead (QGPU_WINDOW)
+    // scheduler A/B knobs (measured no gain on the bench circuit, off):
+    int lane_cap = 0;    // shuffle lane ops per reordered pass (QGPU_LANE_CAP; 0: no cap)
+    int interleave = 0;  // alternate lane ops with the other ops in a phase (QGPU_INTERLEAVE)
+    int normalize = 1;   // unit-coefficient gate normalization in tolerance mode (QGPU_NORMALIZE)
     std::unique_ptr<NcclComm> nccl;
     std::unique_ptr<PeerGroup> peer;
     bool multi_process() const { return mode == Mode::Nccl || mode == Mode::Peer; }
@@ -127,6 +131,9 @@ struct FlatOp {
     uint64_t cmask = 0;
     double m[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     int32_t id = -1; // caller's op index (qgpuPlanPasses dry runs)
+    // unit coefficients of a normalized real / Rx-class gate (tolerance mode,
+    // runtime.cpp normalize_op): 2 bits per coefficient, tile header bits 40-47
+    uint8_t unit = 0;
 };
 
 uint8_t classify(const double* m, uint8_t* diag_flags);
@@ -175,9 +182,16 @@ struct QuregImpl {
     // pass formation. A pass is cut from the window by commutation, not by
     // position (window_pass); pending / phases then hold that pass only.
     std::vector<FlatOp> win;
+    // Scalar factored out of the window's normalized gates (normalize_op),
+    // folded into one op of a later pass (fold_scale); 1 whenever the window
+    // is empty after a drain.
+    double gscale_re = 1.0, gscale_im = 0.0;
+    bool normalize_op(FlatOp& op);
+    bool fold_scale();
     bool reorder_on() const;
     void window_pass();  // form and launch one pass from the window
     void window_drain(); // ... until the window is empty
+    void interleave_lane_ops(int begin, const std::vector<int>& regs);
 
     // Dry run (qgpuPlanPasses): passes are recorded here instead of launched
     struct PlannedPass {
@@ -206,6 +220,8 @@ struct QuregImpl {
     void discard_all() { // queued ops are dead (the state is overwritten)
         lq.clear();
         win.clear();
+        gscale_re = 1.0;
+        gscale_im = 0.0;
         deferred.clear();
         ++version;
         discard();

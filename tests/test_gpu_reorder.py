@@ -228,3 +228,42 @@ def test_30q_bench_circuit_against_reference(env):
             q.destroy()
     finally:
         quest.set_jit(1)
+
+
+def test_scale_folding_paths(env):
+    """Unit-coefficient normalization factors scalars out of uncontrolled
+    H / Rx / Ry / Rz gates; they must be applied exactly once whatever the
+    pass holds: a circuit whose last passes contain only controlled gates
+    (the scalar is appended as its own elementwise op), a read in the middle
+    (the window drains), and a register re-initialised with scalars pending."""
+    n = 14
+    c = C.Circuit(n, 0, [C.GateOp("H", q) for q in range(n)])
+    c.ops += [C.GateOp("RX", q, angle=0.3 + q) for q in range(n)]
+    c.ops += [C.GateOp("RZ", q, angle=1.1 * q) for q in range(n)]
+    c.ops += [C.GateOp("X", (q + 1) % n, (q,)) for q in range(n)]
+    c.ops += [C.GateOp("PHASE", q, ((q + 3) % n,), angle=0.7) for q in range(n)]
+    want = oracle_run(c)
+    q = quest.QuregHandle(env, n)
+    try:
+        C.apply_circuit(q, c)
+        assert max_err(q.state(), want) <= TOL
+        assert abs(q.calcTotalProb() - 1.0) <= 1e-12
+        # gates, then a re-init: pending scalars are dropped with the ops
+        C.apply_circuit(q, c)
+        q.initZeroState()
+        C.apply_circuit(q, c)
+        assert max_err(q.state(), want) <= TOL
+    finally:
+        q.destroy()
+
+
+@pytest.mark.parametrize("angle", [0.0, np.pi, np.pi / 2, 1e-300, np.pi - 1e-15])
+def test_normalization_edge_angles(env, angle):
+    """Rotations whose sine or cosine is zero or tiny (the pivot is the
+    larger of the two, so the factored matrix stays bounded)."""
+    n = 13
+    c = C.Circuit(n, 0, [C.GateOp("H", q) for q in range(n)])
+    for name in ("RX", "RY", "RZ", "PHASE"):
+        c.ops += [C.GateOp(name, q, angle=angle * (1 + (q % 2))) for q in range(n)]
+    got, _ = run(env, c)
+    assert max_err(got, oracle_run(c)) <= TOL

@@ -38,6 +38,37 @@ __global__ void k_lds(double2* out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = acc;
 }
 
+// SHFL and DFMA interleaved, independent: does the shuffle unit overlap the
+// FP64 pipe? (time ~ max of the two alone if so, ~ their sum if not)
+__global__ void k_mix(double* out, int iters) {
+    float a = threadIdx.x, b = a + 1, c = a + 2, d = a + 3;
+    double x = threadIdx.x, y = 1.0000001, c0 = 0.1, c1 = 0.2, c2 = 0.3, c3 = 0.4, c4 = 0.5, c5 = 0.6, c6 = 0.7, c7 = 0.8;
+    for (int i = 0; i < iters; ++i) {
+        a = __shfl_xor_sync(0xffffffffu, a, 1);
+        c0 = fma(x, y, c0); c1 = fma(x, y, c1);
+        b = __shfl_xor_sync(0xffffffffu, b, 2);
+        c2 = fma(x, y, c2); c3 = fma(x, y, c3);
+        c = __shfl_xor_sync(0xffffffffu, c, 4);
+        c4 = fma(x, y, c4); c5 = fma(x, y, c5);
+        d = __shfl_xor_sync(0xffffffffu, d, 8);
+        c6 = fma(x, y, c6); c7 = fma(x, y, c7);
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = a + b + c + d + c0 + c1 + c2 + c3 + c4 + c5 + c6 + c7;
+}
+
+// indexed shuffles (SHFL.IDX with a per-lane source)
+__global__ void k_shfl_idx(float* out, int iters) {
+    float a = threadIdx.x, b = a + 1, c = a + 2, d = a + 3;
+    const int src = (threadIdx.x & 31) ^ ((threadIdx.x >> 2) & 1 ? 4 : 0);
+    for (int i = 0; i < iters; ++i) {
+        a = __shfl_sync(0xffffffffu, a, src);
+        b = __shfl_sync(0xffffffffu, b, src ^ 1);
+        c = __shfl_sync(0xffffffffu, c, src ^ 2);
+        d = __shfl_sync(0xffffffffu, d, src ^ 8);
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = a + b + c + d;
+}
+
 template <class K, class T>
 void run(const char* name, K kern, T* buf, int iters, double instr_per_iter_per_warp, int threads) {
     cudaEvent_t a, b;
@@ -64,5 +95,7 @@ int main() {
     run("SHFL", k_shfl, (float*)buf, 20000, 4, 512);
     run("DFMA", k_dfma, (double*)buf, 20000, 8, 512);
     run("LDS.128", k_lds, (double2*)buf, 20000, 4, 256);
+    run("SHFL.IDX", k_shfl_idx, (float*)buf, 20000, 4, 512);
+    run("MIX", k_mix, (double*)buf, 20000, 12, 512); // 4 SHFL + 8 DFMA per iteration
     return 0;
 }
