@@ -217,6 +217,11 @@ void qgpuJitWait(void);
  * also does it from an atexit handler; the Python wrapper from its own). */
 void qgpuJitShutdown(void);
 void qgpuJitStats(unsigned long long* kernels, unsigned long long* failed, unsigned long long* pending);
+/* Lane <-> register exchange ops the tile passes of this process have
+ * carried so far (a run of pair ops on a lane qubit done in registers
+ * between two exchanges instead of as warp-shuffle ops; QGPU_XCHG=0 turns
+ * them off). A tuning / test counter. */
+unsigned long long qgpuLaneExchanges(void);
 /* Host-only (no GPU): compile a sample pass program for sm_100a with NVRTC.
  * Returns the cubin size, or -1 (message in log); *seconds = compile time. */
 int qgpuJitSelfTest(char* log, int len, double* seconds);

@@ -337,8 +337,9 @@ QuESTEnv make_env(Mode mode, int rank, int nranks, int device, const char* id128
     }
     if (const char* v = std::getenv("QGPU_WINDOW")) e->window = std::clamp(std::atoi(v), 1, 65536);
     if (const char* v = std::getenv("QGPU_LANE_CAP")) e->lane_cap = std::max(0, std::atoi(v));
-    if (const char* v = std::getenv("QGPU_INTERLEAVE")) e->interleave = std::atoi(v) != 0;
     if (const char* v = std::getenv("QGPU_NORMALIZE")) e->normalize = std::atoi(v) != 0;
+    if (const char* v = std::getenv("QGPU_XCHG")) e->exchanges = std::atoi(v);
+    if (const char* v = std::getenv("QGPU_MERGE")) e->merge = std::atoi(v) != 0;
     if (const char* v = std::getenv("QGPU_TILE_PHASES"))
         e->tile_phases = std::clamp(std::atoi(v), 1, qgpu::kMaxPhases);
     if (mode == Mode::Nccl && nranks > 1) e->nccl = std::make_unique<NcclComm>(rank, nranks, id128);
@@ -1283,7 +1284,8 @@ int qgpuPlanPasses(int flatQubits, int numOps, const int* kinds, const int* q0, 
             throw qgpu::DomainError("invalid pass-plan request");
         Env e;
         if (const char* v = std::getenv("QGPU_LANE_CAP")) e.lane_cap = std::max(0, std::atoi(v));
-        if (const char* v = std::getenv("QGPU_INTERLEAVE")) e.interleave = std::atoi(v) != 0;
+        if (const char* v = std::getenv("QGPU_XCHG")) e.exchanges = std::atoi(v);
+        if (const char* v = std::getenv("QGPU_MERGE")) e.merge = std::atoi(v) != 0;
         e.order = reorder ? 1 : 0;
         if (windowOps > 0) e.window = windowOps;
         e.tile_phases = maxPhases;
@@ -1425,5 +1427,7 @@ void qgpuJitStats(unsigned long long* kernels, unsigned long long* failed, unsig
 }
 
 int qgpuJitSelfTest(char* log, int len, double* seconds) { return qgpu::jit_selftest(log, len, seconds); }
+
+unsigned long long qgpuLaneExchanges(void) { return qgpu::g_lane_exchanges.load(); }
 
 } // extern "C"

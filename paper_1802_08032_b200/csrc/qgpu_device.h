@@ -170,6 +170,7 @@ enum TileCode : uint8_t {
     TC_DEPOL = 51, // + register-bit pair (0,1) (0,2) (0,3) (1,2) (1,3) (2,3): 51..56
     TC_DEPOL_LANE = 57, // + register bit of t+N, t on a lane bit: 57..60
     TC_LANE_RX = 61,    // Rx-class 2x2 on a lane bit (tolerance mode only: TileParams.fast)
+    TC_LANE_XCHG = 62,  // exchange lane bit q0 pos with register bit q1 pos (pure moves)
 };
 
 // Op header packed in one 64-bit word (one constant-bank load per op):

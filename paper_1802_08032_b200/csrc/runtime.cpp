@@ -31,6 +31,8 @@
 
 namespace qgpu {
 
+std::atomic<unsigned long long> g_lane_exchanges{0};
+
 cudaError_t memcpy_counted(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind, cudaStream_t s) {
     if (kind == cudaMemcpyHostToDevice) count_transfer(bytes, 0);
     if (kind == cudaMemcpyDeviceToHost) count_transfer(0, bytes);
@@ -379,11 +381,21 @@ bool QuregImpl::place_tile_depol(const FlatOp& op) {
 // unblocks the most ready ops; a phase ends when its registers are full and
 // nothing else fits. Ops the phases could not take stay in the window.
 namespace {
+// How an op acts on each qubit, for commutation: diagonally (controls,
+// diagonal targets, dephasing, collapse), as an X-type 2x2 ([[a, b], [b,
+// a]]: X / CNOT targets, Rx — these commute with each other), or otherwise
+// non-diagonally. Two ops commute when every qubit they share is diagonal
+// in both or X-type in both.
 struct OpQubits {
-    uint64_t nd = 0;   // qubits the op acts on non-diagonally
+    uint64_t nd = 0;   // qubits the op acts on non-diagonally, not X-type
+    uint64_t nx = 0;   // qubits it acts on as an X-type 2x2
     uint64_t dg = 0;   // qubits it acts on diagonally (controls, phases)
     uint64_t need = 0; // qubits that must be in the tile
 };
+bool x_type(const FlatOp& op) {
+    return op.kind == FK_GATE && op.cls != CLS_DIAG && op.m[0] == op.m[6] && op.m[1] == op.m[7] &&
+           op.m[2] == op.m[4] && op.m[3] == op.m[5];
+}
 OpQubits op_qubits(const FlatOp& op) {
     auto bit = [](int q) { return q >= 0 ? uint64_t{1} << q : uint64_t{0}; };
     OpQubits r;
@@ -392,8 +404,8 @@ OpQubits op_qubits(const FlatOp& op) {
         if (op.cls == CLS_DIAG) {
             r.dg |= bit(op.q0);
         } else {
-            r.nd = bit(op.q0);
-            r.need = r.nd;
+            (x_type(op) ? r.nx : r.nd) = bit(op.q0);
+            r.need = bit(op.q0);
         }
     } else if (op.kind == FK_DEPOL) {
         r.nd = bit(op.q0) | bit(op.q1);
@@ -403,8 +415,18 @@ OpQubits op_qubits(const FlatOp& op) {
     }
     return r;
 }
-inline bool blocked_by(const OpQubits& a, uint64_t bnd, uint64_t bdg) {
-    return (a.nd & (bnd | bdg)) != 0 || (a.dg & bnd) != 0;
+// what the ops skipped so far act on (an op may not pass any of them that it
+// does not commute with)
+struct Blockers {
+    uint64_t nd = 0, nx = 0, dg = 0;
+    void add(const OpQubits& o) {
+        nd |= o.nd;
+        nx |= o.nx;
+        dg |= o.dg;
+    }
+};
+inline bool blocked_by(const OpQubits& a, const Blockers& b) {
+    return (a.nd & (b.nd | b.nx | b.dg)) != 0 || (a.nx & (b.nd | b.dg)) != 0 || (a.dg & (b.nd | b.nx)) != 0;
 }
 } // namespace
 
@@ -507,47 +529,57 @@ bool QuregImpl::reorder_on() const {
     return env->order == 1 && use_tile() && env->fusion_mode == 0;
 }
 
-// Reorders pending[begin, end) — one phase — so that shuffle-bound lane ops
-// alternate with the other ops where dependencies allow (list scheduling,
-// earliest ready op of the wanted kind first): the compiler then overlaps a
-// lane op's shuffles with its neighbours' FP64 work in the straight-line
-// JIT program instead of running a burst of lane ops shuffle-bound.
-void QuregImpl::interleave_lane_ops(int begin, const std::vector<int>& R) {
-    const int n = static_cast<int>(pending.size()) - begin;
-    if (n < 3) return;
-    const int lf = lane_fixed();
-    std::vector<OpQubits> oq(n);
-    std::vector<char> lane(n), done(n, 0);
-    int nl = 0;
-    for (int i = 0; i < n; ++i) {
-        const FlatOp& op = pending[begin + i];
-        oq[i] = op_qubits(op);
-        lane[i] = op.kind == FK_GATE && op.cls != CLS_DIAG && op.q0 < kLaneQubits &&
-                  (op.q0 < lf || std::find(R.begin(), R.end(), op.q0) == R.end());
-        nl += lane[i];
-    }
-    if (nl == 0 || nl == n) return;
-    std::vector<FlatOp> out;
-    out.reserve(n);
-    bool want_lane = false;
-    for (int k = 0; k < n; ++k) {
-        int pick = -1, any = -1;
-        uint64_t bnd = 0, bdg = 0;
-        for (int i = 0; i < n; ++i) {
-            if (done[i]) continue;
-            if (!blocked_by(oq[i], bnd, bdg)) {
-                if (any < 0) any = i;
-                if (pick < 0 && lane[i] == want_lane) pick = i;
-            }
-            bnd |= oq[i].nd;
-            bdg |= oq[i].dg;
+// Same-qubit merging (tolerance mode): an uncontrolled 2x2 gate X on qubit q
+// is multiplied into the latest window op Y on q that is itself an
+// uncontrolled 2x2 on q, provided X commutes with every op in between that
+// touches q (op_qubits' rule: diagonal with diagonal, X-type with X-type) and
+// the product stays a cheap class (diagonal, real or Rx-class: Rz Rz, Rx Rx
+// across CNOT targets, Ry Ry, ...; a complex 2x2 costs more than the two
+// rotations). Y then applies X Y at Y's place — X moved across ops it
+// commutes with. Dry runs record X's id after Y's (merged_ids).
+bool QuregImpl::merge_into_window(const FlatOp& x) {
+    if (x.kind != FK_GATE || x.cmask != 0 || win.empty()) return false;
+    const OpQubits xo = op_qubits(x);
+    const uint64_t qb = uint64_t{1} << x.q0;
+    for (size_t k = win.size(); k-- > 0;) {
+        FlatOp& y = win[k];
+        const OpQubits yo = op_qubits(y);
+        if (!((yo.nd | yo.nx | yo.dg) & qb)) continue;
+        if (y.kind == FK_GATE && y.cmask == 0 && y.q0 == x.q0) {
+            // product X * Y (X applied after Y), complex 2x2 row-major
+            double p[8];
+            for (int r = 0; r < 2; ++r)
+                for (int c = 0; c < 2; ++c) {
+                    double re = 0.0, im = 0.0;
+                    for (int j = 0; j < 2; ++j) {
+                        const double ar = x.m[4 * r + 2 * j], ai = x.m[4 * r + 2 * j + 1];
+                        const double br = y.m[4 * j + 2 * c], bi = y.m[4 * j + 2 * c + 1];
+                        re += ar * br - ai * bi;
+                        im += ar * bi + ai * br;
+                    }
+                    p[4 * r + 2 * c] = re;
+                    p[4 * r + 2 * c + 1] = im;
+                }
+            uint8_t flags = 0;
+            const uint8_t cls = classify(p, &flags);
+            if (cls == CLS_GENERIC || cls == CLS_SWAP) return false;
+            std::memcpy(y.m, p, sizeof(p));
+            y.cls = cls;
+            y.flags = flags;
+            y.unit = 0;
+            // Y's old scalar is already in gscale; this takes X's in
+            if (env->normalize) normalize_op(y);
+            if (plan_sink && x.id >= 0) merged_ids[y.id].push_back(x.id);
+            return true;
         }
-        if (pick < 0) pick = any;
-        done[pick] = 1;
-        out.push_back(pending[begin + pick]);
-        want_lane = !lane[pick];
+        if (blocked_by(xo, [&] {
+                Blockers b;
+                b.add(yo);
+                return b;
+            }()))
+            return false;
     }
-    std::copy(out.begin(), out.end(), pending.begin() + begin);
+    return false;
 }
 
 void QuregImpl::window_drain() {
@@ -567,16 +599,15 @@ void QuregImpl::window_pass() {
     cand &= ~lanes;
     // ops a tile of qubits T admits: one ordered scan
     auto closure = [&](uint64_t T, std::vector<char>* sel) {
-        uint64_t bnd = 0, bdg = 0;
+        Blockers bl;
         int n = 0;
         for (size_t j = 0; j < W; ++j) {
             const OpQubits& o = oq[j];
-            const bool ok = (o.need & ~T) == 0 && !blocked_by(o, bnd, bdg);
+            const bool ok = (o.need & ~T) == 0 && !blocked_by(o, bl);
             if (ok) {
                 ++n;
             } else {
-                bnd |= o.nd;
-                bdg |= o.dg;
+                bl.add(o);
             }
             if (sel) (*sel)[j] = ok ? 1 : 0;
         }
@@ -634,6 +665,7 @@ void QuregImpl::window_pass() {
         if (op.q0 < lf) return true;
         return !in(R, op.q0) && static_cast<int>(R.size()) >= kPhaseRegBits; // 3, 4 as lane bits
     };
+    std::vector<size_t> pwin; // window index of each pending op
     while (static_cast<int>(phases.size()) < maxph && pending.size() < cap) {
         PhaseState ph;
         ph.op_begin = static_cast<int>(pending.size());
@@ -643,12 +675,12 @@ void QuregImpl::window_pass() {
             bool progress = true;
             while (progress && pending.size() < cap) {
                 progress = false;
-                uint64_t bnd = 0, bdg = 0;
+                Blockers bl;
                 for (size_t j = 0; j < W; ++j) {
                     if (!sel[j] || taken[j]) continue;
                     int qs[2];
                     const bool lane = shuffles(j, R);
-                    if (pending.size() < cap && !blocked_by(oq[j], bnd, bdg) && missing(j, R, qs) == 0 &&
+                    if (pending.size() < cap && !blocked_by(oq[j], bl) && missing(j, R, qs) == 0 &&
                         !(lane && env->lane_cap > 0 && lane_ops >= env->lane_cap)) {
                         const FlatOp& op = win[j];
                         if (lane) ++lane_ops;
@@ -658,11 +690,11 @@ void QuregImpl::window_pass() {
                             !in(R, op.q0) && static_cast<int>(R.size()) < kPhaseRegBits)
                             R.push_back(op.q0);
                         pending.push_back(op);
+                        pwin.push_back(j);
                         taken[j] = 1;
                         progress = any = true;
                     } else {
-                        bnd |= oq[j].nd;
-                        bdg |= oq[j].dg;
+                        bl.add(oq[j]);
                     }
                 }
             }
@@ -670,17 +702,16 @@ void QuregImpl::window_pass() {
             if (pending.size() >= cap || room <= 0) break;
             // the register qubit that unblocks the most ready ops
             int cnt[64] = {};
-            uint64_t bnd = 0, bdg = 0;
+            Blockers bl;
             for (size_t j = 0; j < W; ++j) {
                 if (!sel[j] || taken[j]) continue;
-                if (!blocked_by(oq[j], bnd, bdg)) {
+                if (!blocked_by(oq[j], bl)) {
                     int qs[2];
                     const int k = missing(j, R, qs);
                     if (k > 0 && k <= room)
                         for (int i = 0; i < k; ++i) ++cnt[qs[i]];
                 }
-                bnd |= oq[j].nd;
-                bdg |= oq[j].dg;
+                bl.add(oq[j]);
             }
             int bq = -1;
             for (int q = 0; q < 64; ++q)
@@ -689,10 +720,37 @@ void QuregImpl::window_pass() {
             R.push_back(bq);
         }
         if (!any) break;
-        if (env->interleave) interleave_lane_ops(ph.op_begin, R);
         phases.push_back(ph);
     }
     if (pending.empty()) throw DeviceError("internal: reorder scheduler formed an empty pass");
+    // Room for the lane <-> register exchanges launch_tile adds (two per lane
+    // qubit with two or more pair ops in a phase, at most one per register
+    // bit): the pass's last ops go back to the window if needed (a suffix of
+    // a dependency-ordered list: nothing kept depends on them).
+    auto xneed = [&]() {
+        if (env->exchanges != 1) return 0; // (2: exchanges only where a pass has room)
+        int need = 0;
+        for (size_t p = 0; p < phases.size(); ++p) {
+            const size_t b = static_cast<size_t>(phases[p].op_begin);
+            const size_t e = p + 1 < phases.size() ? static_cast<size_t>(phases[p + 1].op_begin) : pending.size();
+            int cnt[kLaneQubits] = {};
+            for (size_t k = b; k < e; ++k) {
+                const FlatOp& op = pending[k];
+                if (op.kind == FK_GATE && op.cls != CLS_DIAG && op.q0 < kLaneQubits && !in(phases[p].regs, op.q0))
+                    ++cnt[op.q0];
+            }
+            int c = 0;
+            for (int q = 0; q < kLaneQubits; ++q) c += cnt[q] >= 2;
+            need += 2 * std::min(c, kPhaseRegBits);
+        }
+        return need;
+    };
+    while (pending.size() > 1 && static_cast<int>(pending.size()) + xneed() > kMaxTileOps) {
+        taken[pwin.back()] = 0;
+        pwin.pop_back();
+        pending.pop_back();
+        if (phases.size() > 1 && static_cast<size_t>(phases.back().op_begin) >= pending.size()) phases.pop_back();
+    }
     for (const PhaseState& ph : phases)
         for (int q : ph.regs)
             if (q >= kLaneQubits && !in(tile_high, q)) tile_high.push_back(q);
@@ -787,6 +845,7 @@ void QuregImpl::enqueue_phys(const FlatOp& op) {
                                   ? op.q1 >= lane_fixed() && op.q0 < local_qubits && op.q1 < local_qubits
                                   : !(pair && op.q0 >= local_qubits);
         if (tileable) {
+            if (env->merge && merge_into_window(op)) return;
             win.push_back(op);
             if (env->normalize) normalize_op(win.back());
             if (static_cast<int>(win.size()) >= env->window) window_pass();
@@ -963,8 +1022,16 @@ int pass_profile_info(const TileParams& P) {
 void QuregImpl::launch_tile() {
     if (plan_sink) {
         PlannedPass pp;
-        for (const FlatOp& op : pending) pp.ids.push_back(op.id);
-        for (const PhaseState& ph : phases) pp.phase_begin.push_back(ph.op_begin);
+        std::vector<int> at(pending.size() + 1, 0); // index into ids of each pending op
+        for (size_t k = 0; k < pending.size(); ++k) {
+            at[k] = static_cast<int>(pp.ids.size());
+            pp.ids.push_back(pending[k].id);
+            auto it = merged_ids.find(pending[k].id);
+            if (it != merged_ids.end())
+                for (int id : it->second) pp.ids.push_back(id);
+        }
+        at[pending.size()] = static_cast<int>(pp.ids.size());
+        for (const PhaseState& ph : phases) pp.phase_begin.push_back(at[ph.op_begin]);
         plan_sink->push_back(std::move(pp));
         ++passes;
         return;
@@ -1159,6 +1226,84 @@ void QuregImpl::launch_tile() {
         while (run < kTileHigh - kTileWarpBits && high[run] == kLaneQubits + run) ++run;
         P.fin_run = run;
     }
+    // Lane <-> register exchanges for one phase's ops [begin, end): a lane
+    // qubit (a tile bit on lane bits 0-4) with two or more pair ops in the
+    // phase moves to a register bit J for the run from its first to its last
+    // pair op, and back after it (TC_LANE_XCHG: half a lane op's shuffles
+    // each), so those ops run as register ops instead of shuffle-bound lane
+    // ops. J's qubit must have no pair op or depolarising channel inside the
+    // run (it sits on the lane bit meanwhile; its diagonal ops and controls
+    // work there). Returns the phase's emitted sequence: pending indices, and
+    // exchanges encoded as -1 - (b * kPhaseRegBits + J). `room`: ops the pass
+    // can still take (two per exchange). Pure moves: exact in both modes.
+    auto plan_exchanges = [&](int begin, int end, const int* lane_t, const int* reg_t, int room) {
+        auto pair_t = [&](const FlatOp& op) { // the tile bit an op pairs on (-1: none)
+            return op.kind == FK_GATE && op.cls != CLS_DIAG ? tbit(op.q0) : -1;
+        };
+        struct X {
+            int b, J, first, last;
+        };
+        std::vector<X> xs;
+        bool depol = false;
+        for (int k = begin; k < end; ++k) depol |= pending[k].kind == FK_DEPOL;
+        if (env->exchanges && room >= 2 && !depol) {
+            // Greedy over intervals: lane bit b's qubit sits on register bit J
+            // from its use u_i to its use u_j (both pair ops on it), while J's
+            // qubit waits on lane bit b (its pair ops there become lane ops).
+            // Benefit in lane ops: (j - i + 1) - (J's pair ops inside) - 1
+            // (the two exchanges: half a lane op each). Intervals sharing a
+            // lane bit or a register bit must not overlap.
+            std::vector<int> uses[kLaneQubits], busy[kPhaseRegBits];
+            for (int k = begin; k < end; ++k) {
+                const int t = pair_t(pending[k]);
+                for (int b = 0; b < kLaneQubits; ++b)
+                    if (t == lane_t[b]) uses[b].push_back(k);
+                for (int J = 0; J < kPhaseRegBits; ++J)
+                    if (t == reg_t[J]) busy[J].push_back(k);
+            }
+            auto overlaps = [](const X& x, int f, int l) { return !(x.last < f || l < x.first); };
+            for (;;) {
+                int best = 0;
+                X bx{-1, -1, -1, -1};
+                for (int b = 0; b < kLaneQubits; ++b) {
+                    const std::vector<int>& u = uses[b];
+                    for (size_t i = 0; i < u.size(); ++i)
+                        for (size_t j = i + 1; j < u.size(); ++j) {
+                            bool lane_free = true;
+                            for (const X& x : xs)
+                                if (x.b == b && overlaps(x, u[i], u[j])) lane_free = false;
+                            if (!lane_free) break; // (longer runs overlap too)
+                            for (int J = 0; J < kPhaseRegBits; ++J) {
+                                bool free = true;
+                                for (const X& x : xs)
+                                    if (x.J == J && overlaps(x, u[i], u[j])) free = false;
+                                if (!free) continue;
+                                int inside = 0;
+                                for (int k : busy[J]) inside += k > u[i] && k < u[j];
+                                const int gain = static_cast<int>(j - i + 1) - inside - 1;
+                                if (gain > best) {
+                                    best = gain;
+                                    bx = X{b, J, u[i], u[j]};
+                                }
+                            }
+                        }
+                }
+                if (best <= 0 || room < 2) break;
+                xs.push_back(bx);
+                room -= 2;
+            }
+        }
+        std::vector<int> seq;
+        for (int k = begin; k < end; ++k) {
+            for (const X& x : xs)
+                if (x.first == k) seq.push_back(-1 - (x.b * kPhaseRegBits + x.J));
+            seq.push_back(k);
+            for (const X& x : xs)
+                if (x.last == k) seq.push_back(-1 - (x.b * kPhaseRegBits + x.J));
+        }
+        return seq;
+    };
+    int ko = 0, xchg_used = 0; // emitted ops, exchanges among them
     for (size_t p = 0; p < phases.size(); ++p) {
         TilePhase& Q = P.phases[p];
         const std::vector<int>& rb = RB[p];
@@ -1234,43 +1379,54 @@ void QuregImpl::launch_tile() {
         }
         const int begin = phases[p].op_begin;
         const int end = p + 1 < phases.size() ? phases[p + 1].op_begin : static_cast<int>(pending.size());
-        Q.op_begin = static_cast<uint16_t>(begin);
-        Q.op_end = static_cast<uint16_t>(end);
+        // Where each tile bit sits while the phase's ops run: lane bits 0-4
+        // and register bits, updated by lane <-> register exchanges
+        // (plan_exchanges: a run of pair ops on a lane qubit runs on a
+        // register bit between two exchanges instead of as shuffle ops).
+        int cur_lane[kLaneQubits] = {0, 1, 2, lb[0], lb[1]};
+        int cur_reg[kPhaseRegBits];
+        for (int j = 0; j < kPhaseRegBits; ++j) cur_reg[j] = rb[j];
+        const int xroom = kMaxTileOps - static_cast<int>(pending.size()) - xchg_used;
+        const std::vector<int> seq = plan_exchanges(begin, end, cur_lane, cur_reg, xroom);
+        Q.op_begin = static_cast<uint16_t>(ko);
         auto loc = [&](int q, uint8_t* kind, uint8_t* pos) {
             const int t = tbit(q);
-            if (q < 0) {
-                *kind = TL_OUTER;
-                *pos = 0;
-            } else if (t < 0) {
-                *kind = TL_OUTER;
-                *pos = static_cast<uint8_t>(q);
-            } else if (t < kFixedLaneBits) {
-                *kind = TL_LANE;
-                *pos = static_cast<uint8_t>(t);
-            } else {
-                for (int j = 0; j < 2; ++j)
-                    if (lb[j] == t) {
-                        *kind = TL_LANE;
-                        *pos = static_cast<uint8_t>(kFixedLaneBits + j);
-                        return;
-                    }
-                for (int j = 0; j < kPhaseRegBits; ++j)
-                    if (rb[j] == t) {
-                        *kind = TL_REG;
-                        *pos = static_cast<uint8_t>(j);
-                        return;
-                    }
-                for (int j = 0; j < kTileWarpBits; ++j)
-                    if (wb[j] == t) {
-                        *kind = TL_WARP;
-                        *pos = static_cast<uint8_t>(j);
-                        return;
-                    }
-            }
+            *kind = TL_OUTER;
+            *pos = static_cast<uint8_t>(q < 0 ? 0 : q);
+            if (q < 0 || t < 0) return;
+            for (int j = 0; j < kLaneQubits; ++j)
+                if (cur_lane[j] == t) {
+                    *kind = TL_LANE;
+                    *pos = static_cast<uint8_t>(j);
+                    return;
+                }
+            for (int j = 0; j < kPhaseRegBits; ++j)
+                if (cur_reg[j] == t) {
+                    *kind = TL_REG;
+                    *pos = static_cast<uint8_t>(j);
+                    return;
+                }
+            for (int j = 0; j < kTileWarpBits; ++j)
+                if (wb[j] == t) {
+                    *kind = TL_WARP;
+                    *pos = static_cast<uint8_t>(j);
+                    return;
+                }
         };
-        for (int k = begin; k < end; ++k) {
-            const FlatOp& op = pending[k];
-            TileOp& to = P.ops[k];
+        for (const int e : seq) {
+            TileOp& to = P.ops[ko++];
+            if (e < 0) { // exchange: lane bit b <-> register bit J (encoded -1 - (b * 4 + J))
+                const int b = (-1 - e) / kPhaseRegBits, J = (-1 - e) % kPhaseRegBits;
+                std::swap(cur_lane[b], cur_reg[J]);
+                ++xchg_used;
+                if (!plan_sink) ++g_lane_exchanges;
+                to.hdr = tile_hdr(TC_LANE_XCHG, 0, 0, TL_LANE, static_cast<uint32_t>(b), TL_REG,
+                                  static_cast<uint32_t>(J), 0, 0, 0);
+                to.outer_cmask = 0;
+                std::memset(to.m, 0, sizeof(to.m));
+                continue;
+            }
+            const FlatOp& op = pending[e];
             const uint32_t flags = op.kind == FK_COLLAPSE ? (op.q1 >= 0 ? 1 : 0) : op.flags;
             uint8_t q0k = 0, q0p = 0, q1k = 0, q1p = 0;
             loc(op.q0, &q0k, &q0p);
@@ -1343,13 +1499,18 @@ void QuregImpl::launch_tile() {
             if (outer) P.any_outer = 1;
             std::memcpy(to.m, op.m, sizeof(to.m));
         }
+        for (int j = 0; j < kLaneQubits; ++j)
+            if (cur_lane[j] != (j < kFixedLaneBits ? j : lb[j - kFixedLaneBits]))
+                throw DeviceError("internal: a lane exchange was not undone within its phase");
+        Q.op_end = static_cast<uint16_t>(ko);
     }
     // Bits every op needs at 1 outside the tile: local ones shrink the tile
     // enumeration (the other tiles are left untouched in HBM: a lone
     // controlled gate reads and writes half the state), rank ones skip the
     // shard (the reference's rank-id control skip, distributed.cpp:143-145)
     uint64_t common = ~uint64_t{0};
-    for (int k = 0; k < P.phases[P.num_phases - 1].op_end; ++k) common &= P.ops[k].outer_cmask;
+    for (int k = 0; k < P.phases[P.num_phases - 1].op_end; ++k)
+        if ((P.ops[k].hdr & 63) != TC_LANE_XCHG) common &= P.ops[k].outer_cmask; // (exchanges: pure moves)
     const uint64_t local_mask = local_len - 1;
     P.skip_ones = common & local_mask;
     const uint64_t rank_need = common & ~local_mask;

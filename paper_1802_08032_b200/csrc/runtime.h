@@ -10,9 +10,11 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
 #include <set>
+#include <unordered_map>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -75,8 +77,13 @@ struct Env {
     int window = 512; // ops the reorder scheduler looks ahead (QGPU_WINDOW)
     // scheduler A/B knobs (measured no gain on the bench circuit, off):
     int lane_cap = 0;    // shuffle lane ops per reordered pass (QGPU_LANE_CAP; 0: no cap)
-    int interleave = 0;  // alternate lane ops with the other ops in a phase (QGPU_INTERLEAVE)
     int normalize = 1;   // unit-coefficient gate normalization in tolerance mode (QGPU_NORMALIZE)
+    int merge = 1;       // same-qubit gate merging in the reorder window (QGPU_MERGE)
+    // lane <-> register exchanges around runs of lane-qubit pair ops (QGPU_XCHG:
+    // 1 with room reserved in reordered passes, 2 where a pass has room; off:
+    // measured slower on the bench circuit, the per-element selects of an
+    // exchange cost more ALU issue than the shuffles they save)
+    int exchanges = 0;
     std::unique_ptr<NcclComm> nccl;
     std::unique_ptr<PeerGroup> peer;
     bool multi_process() const { return mode == Mode::Nccl || mode == Mode::Peer; }
@@ -122,6 +129,9 @@ enum FlatKind : uint8_t { FK_GATE = 0, FK_DEPHASE = 1, FK_DEPOL = 2, FK_COLLAPSE
 
 // An operation on the flat 2^flat vector (the reference's FlatGateOp,
 // distributed.hpp:78-85, extended with the channels and collapse).
+// lane <-> register exchange ops emitted by tile passes (qgpuLaneExchanges)
+extern std::atomic<unsigned long long> g_lane_exchanges;
+
 struct FlatOp {
     uint8_t kind = FK_GATE;
     uint8_t cls = CLS_GENERIC;
@@ -187,11 +197,12 @@ struct QuregImpl {
     // is empty after a drain.
     double gscale_re = 1.0, gscale_im = 0.0;
     bool normalize_op(FlatOp& op);
+    bool merge_into_window(const FlatOp& op);
+    std::unordered_map<int, std::vector<int>> merged_ids; // dry runs: ids merged into an op
     bool fold_scale();
     bool reorder_on() const;
     void window_pass();  // form and launch one pass from the window
     void window_drain(); // ... until the window is empty
-    void interleave_lane_ops(int begin, const std::vector<int>& regs);
 
     // Dry run (qgpuPlanPasses): passes are recorded here instead of launched
     struct PlannedPass {

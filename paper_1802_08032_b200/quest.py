@@ -179,6 +179,7 @@ _SIGS = {
     "qgpuJitShutdown": (None, []),
     "qgpuRunCircuit": (None, [Qureg, _VP, _I]),
     "qgpuJitStats": (None, [_VP, _VP, _VP]),
+    "qgpuLaneExchanges": (ctypes.c_ulonglong, []),
     "qgpuJitSelfTest": (_I, [ctypes.c_char_p, _I, ctypes.POINTER(ctypes.c_double)]),
     "qgpuProfileStart": (None, [QuESTEnv]),
     "qgpuProfileStop": (_I, [QuESTEnv, _VP, _VP, _I]),
@@ -547,6 +548,11 @@ def set_jit(mode: int):
 
 def jit_wait():
     call("qgpuJitWait")
+
+
+def lane_exchanges() -> int:
+    """Lane <-> register exchange ops emitted by tile passes so far."""
+    return int(lib().qgpuLaneExchanges())
 
 
 def jit_stats() -> tuple[int, int, int]:

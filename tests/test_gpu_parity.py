@@ -432,6 +432,47 @@ def test_jit_passes_bit_identical(env, jit_sync, n):
     assert quest.jit_stats()[1] == 0
 
 
+def low_qubit_circuit(n, count, seed):
+    """Random gates whose targets mostly sit on qubits 0-4 (the tile's lane
+    qubits), with controls anywhere: runs of pair ops per lane qubit."""
+    from tests.harness import random_unitary
+
+    rng = np.random.default_rng(seed)
+    names = ["H", "X", "SX", "RX", "RY", "RZ", "T", "U"]
+    c = C.Circuit(n, 0, [])
+    for _ in range(count):
+        t = int(rng.integers(0, 5)) if rng.random() < 0.7 else int(rng.integers(n))
+        others = [q for q in range(n) if q != t]
+        k = int(rng.integers(0, 3)) if rng.random() < 0.3 else 0
+        ctrls = tuple(int(x) for x in rng.choice(others, size=k, replace=False)) if k else ()
+        name = str(rng.choice(names))
+        if name == "U":
+            c.ops.append(C.GateOp("U", t, ctrls, matrix=tuple(random_unitary(rng))))
+        else:
+            c.ops.append(C.GateOp(name, t, ctrls, angle=float(rng.uniform(-2 * np.pi, 2 * np.pi))))
+    return c
+
+
+@pytest.mark.parametrize("jit", [2, 0])
+@pytest.mark.parametrize("n", [13, 18])
+def test_lane_exchanges_bit_identical(monkeypatch, n, jit):
+    """Runs of pair ops on a lane qubit go through lane <-> register
+    exchanges (QGPU_XCHG=2, TC_LANE_XCHG: the qubit moves to a register bit
+    and back, pure moves), so those ops run as register ops: circuit order
+    stays bit for bit the oracle's, JIT (sync) and interpreter."""
+    monkeypatch.setenv("QGPU_XCHG", "2")
+    e = quest.Env()
+    quest.set_jit(jit)
+    try:
+        before = quest.lane_exchanges()
+        c = low_qubit_circuit(n, 240, seed=70 + n)
+        assert_parity(run_product(e, c), oracle_run(c))
+        assert quest.lane_exchanges() > before  # the exchanges were used
+    finally:
+        quest.set_jit(1)
+        e.destroy()
+
+
 @pytest.mark.parametrize("phases", ["3", "8"])
 @pytest.mark.parametrize("n", [20, 22])
 def test_jit_equals_interpreter_multi_phase(monkeypatch, n, phases):

@@ -43,20 +43,31 @@ def flat_ops(circuit: C.Circuit, density: bool = False):
 
 
 def acts(op):
+    """(non-diagonal, X-type, diagonal) qubit masks of an op: two ops commute
+    when every qubit they share is diagonal in both or X-type ([[a, b], [b,
+    a]]: X / CNOT targets, Rx) in both (runtime.cpp op_qubits)."""
     kind, q0, q1, cmask, m = op
-    nd, dg = 0, 0
+    nd, nx, dg = 0, 0, 0
     if kind == 0:
         dg = cmask
         diag = m[2] == 0 and m[3] == 0 and m[4] == 0 and m[5] == 0
         if diag:
             dg |= 1 << q0
+        elif m[0] == m[6] and m[1] == m[7] and m[2] == m[4] and m[3] == m[5]:
+            nx |= 1 << q0
         else:
             nd |= 1 << q0
     elif kind == 2:
         nd = (1 << q0) | (1 << q1)
     else:
         dg = (1 << q0) | ((1 << q1) if q1 >= 0 else 0)
-    return nd, dg
+    return nd, nx, dg
+
+
+def commute(a, b):
+    nda, nxa, dga = a
+    ndb, nxb, dgb = b
+    return not ((nda & (ndb | nxb | dgb)) or (nxa & (ndb | dgb)) or (dga & (ndb | nxb)))
 
 
 def assert_respects_dependencies(ops, order):
@@ -64,10 +75,8 @@ def assert_respects_dependencies(ops, order):
     pos[order] = np.arange(len(ops))
     a = [acts(o) for o in ops]
     for j in range(len(ops)):
-        ndj, dgj = a[j]
         for i in range(j):
-            ndi, dgi = a[i]
-            if (ndi & (ndj | dgj)) or (dgi & ndj):
+            if not commute(a[i], a[j]):
                 assert pos[i] < pos[j], f"op {j} ran before op {i} it does not commute with"
 
 
