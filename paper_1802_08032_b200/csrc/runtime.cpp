@@ -996,8 +996,11 @@ int pass_profile_info(const TileParams& P) {
         } else if (code == TC_LANE_GENERIC || code == TC_LANE_SEL_GENERIC) {
             f = 8.0;
         } else if (code == TC_LANE_REAL || code == TC_LANE_RX) {
-            const bool uni = (u(1) && u(1) == u(2)) || (u(0) && u(0) == u(3));
+            // a unit M (m00, m11) or T (m01, m10) on both rows: one FMA per component (lin2)
+            const bool uni = (u(1) && u(2)) || (u(0) && u(3));
             f = uni ? 2.0 : 4.0;
+        } else if (code == TC_LANE_XCHG) {
+            f = 0.0;
         } else if (code == TC_LANE_SWAP || code == TC_LANE_SEL_SWAP) {
             f = 0.0;
         } else if ((code >= TC_DIAG_REG_D && code < TC_DIAG_REG_D + 4) ||

@@ -75,8 +75,11 @@ struct Env {
     // 0 keeps circuit order (bit-identical to the reference)
     int order = 1;
     int window = 512; // ops the reorder scheduler looks ahead (QGPU_WINDOW)
-    // scheduler A/B knobs (measured no gain on the bench circuit, off):
-    int lane_cap = 0;    // shuffle lane ops per reordered pass (QGPU_LANE_CAP; 0: no cap)
+    // shuffle lane ops per reordered pass (QGPU_LANE_CAP; 0: no cap): capped,
+    // they spread over passes where the shuffle unit idles instead of making
+    // two or three passes shuffle-bound (30q bench: 162.9 vs 165.3 ms/step
+    // uncapped, cap 12: 165.3; profiles/r2/r2y)
+    int lane_cap = 8;
     int normalize = 1;   // unit-coefficient gate normalization in tolerance mode (QGPU_NORMALIZE)
     int merge = 1;       // same-qubit gate merging in the reorder window (QGPU_MERGE)
     // lane <-> register exchanges around runs of lane-qubit pair ops (QGPU_XCHG:
