@@ -337,7 +337,7 @@ QuESTEnv make_env(Mode mode, int rank, int nranks, int device, const char* id128
     }
     if (const char* v = std::getenv("QGPU_WINDOW")) e->window = std::clamp(std::atoi(v), 1, 65536);
     if (const char* v = std::getenv("QGPU_LANE_CAP")) e->lane_cap = std::max(0, std::atoi(v));
-    if (const char* v = std::getenv("QGPU_NORMALIZE")) e->normalize = std::atoi(v) != 0;
+    if (const char* v = std::getenv("QGPU_NORMALIZE")) e->normalize = std::atoi(v); // (2: no symmetric lane diagonals)
     if (const char* v = std::getenv("QGPU_XCHG")) e->exchanges = std::atoi(v);
     if (const char* v = std::getenv("QGPU_MERGE")) e->merge = std::atoi(v) != 0;
     if (const char* v = std::getenv("QGPU_TILE_PHASES"))

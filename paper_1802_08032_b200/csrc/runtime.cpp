@@ -446,17 +446,36 @@ bool QuregImpl::normalize_op(FlatOp& op) {
     double* m = op.m;
     double vr, vi;
     if (op.cls == CLS_DIAG) {
-        if (op.flags & DF_A_ONE) return false;
         const double ar = m[0], ai = m[1], den = ar * ar + ai * ai;
         if (!(den > 0.0)) return false;
         const double dr = (m[6] * ar + m[7] * ai) / den, di = (m[7] * ar - m[6] * ai) / den;
-        vr = ar;
-        vi = ai;
-        m[0] = 1.0;
-        m[1] = 0.0;
-        m[6] = dr;
-        m[7] = di;
-        op.flags = DF_A_ONE | ((dr == 1.0 && di == 0.0) ? DF_D_ONE : 0);
+        if (env->normalize == 1 && op.q0 < lane_fixed() && std::fabs(dr * dr + di * di - 1.0) < 1e-14 &&
+            dr > -0.999) {
+            // On a fixed lane qubit every lane multiplies by its side's factor,
+            // so the identity side of diag(1, r) still costs a complex product.
+            // Symmetric form instead: diag(1, r) = s diag(1 - it, 1 + it) with
+            // t = tan(arg(r) / 2), s = 1 / (1 - it): unit real parts, two FMAs
+            // per amplitude on both sides (unit bit 0: h_diag_lane_fast).
+            const double t = di / (1.0 + dr), q = 1.0 / (1.0 + t * t);
+            const double sr = q, si = t * q; // 1 / (1 - it) = (1 + it) / (1 + t^2)
+            vr = ar * sr - ai * si;
+            vi = ar * si + ai * sr;
+            m[0] = 1.0;
+            m[1] = -t;
+            m[6] = 1.0;
+            m[7] = t;
+            op.flags = 0;
+            op.unit = 1; // real parts exactly 1
+        } else {
+            if (op.flags & DF_A_ONE) return false;
+            vr = ar;
+            vi = ai;
+            m[0] = 1.0;
+            m[1] = 0.0;
+            m[6] = dr;
+            m[7] = di;
+            op.flags = DF_A_ONE | ((dr == 1.0 && di == 0.0) ? DF_D_ONE : 0);
+        }
     } else if (op.cls == CLS_REAL || op.cls == CLS_RX) {
         static const int kReal[4] = {0, 2, 4, 6}, kRx[4] = {0, 3, 5, 6};
         const int* idx = op.cls == CLS_REAL ? kReal : kRx;
@@ -505,11 +524,8 @@ bool QuregImpl::fold_scale() {
     if (best < 0) return false;
     FlatOp& op = pending[best];
     const double sr = gscale_re, si = gscale_im;
-    if (op.cls == CLS_REAL || op.cls == CLS_RX) {
-        // expand the unit entries back to their values (they were exact)
-        op.unit = 0;
-        if (si != 0.0) op.cls = CLS_GENERIC;
-    }
+    op.unit = 0; // the unit entries take the scalar (they were exact)
+    if ((op.cls == CLS_REAL || op.cls == CLS_RX) && si != 0.0) op.cls = CLS_GENERIC;
     for (int k = 0; k < 8; k += 2) {
         const double a = op.m[k], b = op.m[k + 1];
         op.m[k] = a * sr - b * si;
@@ -1008,6 +1024,8 @@ int pass_profile_info(const TileParams& P) {
             f = 2.0; // only the bit-1 half
         } else if (code == TC_DIAG_UNIFORM || code == TC_DIAG_UNIFORM_SEL) {
             f = (flags & (DF_A_ONE | DF_D_ONE)) ? 2.0 : 4.0;
+        } else if (code == TC_DIAG_LANE && u(0) == 1) {
+            f = 2.0; // symmetric form: two FMAs
         } else if (code == TC_DEPHASE || code == TC_COLLAPSE) {
             f = 2.0;
         } else if (code >= TC_DEPOL && code < TC_DEPOL_LANE + 4) {
