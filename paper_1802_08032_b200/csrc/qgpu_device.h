@@ -150,33 +150,37 @@ enum TileLoc : uint8_t { TL_LANE = 0, TL_REG = 1, TL_WARP = 2, TL_OUTER = 3 };
 // carry controls on lane or register qubits (a per-element predicate);
 // controls on warp or outer qubits are uniform per warp and skip the op.
 enum TileCode : uint8_t {
-    TC_REG = 0,      // + 4 * {GENERIC, REAL, RX, SWAP} + register bit: 0..15
-    TC_REG_SEL = 16, // + 4 * {GENERIC, SWAP} + register bit: 16..23
-    TC_LANE_GENERIC = 24,
-    TC_LANE_REAL = 25,
-    TC_LANE_SWAP = 26,
-    TC_LANE_SEL_GENERIC = 27,
-    TC_LANE_SEL_SWAP = 28,
-    TC_DIAG_REG = 29,       // + register bit: both sides (Rz, diag(a, d))
-    TC_DIAG_REG_D = 33,     // + register bit: a == 1 (Z, S, T, phase shift)
-    TC_DIAG_REG_SEL = 37,   // + register bit
-    TC_DIAG_REG_D_SEL = 41, // + register bit
-    TC_DIAG_LANE = 45,      // target on a lane qubit
-    TC_DIAG_LANE_SEL = 46,
-    TC_DIAG_UNIFORM = 47,   // target on a warp / outer qubit
-    TC_DIAG_UNIFORM_SEL = 48,
-    TC_DEPHASE = 49,
-    TC_COLLAPSE = 50,
-    TC_DEPOL = 51, // + register-bit pair (0,1) (0,2) (0,3) (1,2) (1,3) (2,3): 51..56
-    TC_DEPOL_LANE = 57, // + register bit of t+N, t on a lane bit: 57..60
-    TC_LANE_RX = 61,    // Rx-class 2x2 on a lane bit (tolerance mode only: TileParams.fast)
-    TC_LANE_XCHG = 62,  // exchange lane bit q0 pos with register bit q1 pos (pure moves)
+    // register-bit handlers take the bit from the header (q0 pos; q1 pos for
+    // the second qubit of a channel), a literal in JIT programs
+    TC_REG = 0,      // + {GENERIC, REAL, RX, SWAP}: 0..3
+    TC_REG_SEL = 4,  // + {GENERIC, SWAP}: 4..5
+    TC_LANE_GENERIC = 6,
+    TC_LANE_REAL = 7,
+    TC_LANE_SWAP = 8,
+    TC_LANE_SEL_GENERIC = 9,
+    TC_LANE_SEL_SWAP = 10,
+    TC_DIAG_REG = 11,       // both sides (Rz, diag(a, d))
+    TC_DIAG_REG_D = 12,     // a == 1 (Z, S, T, phase shift)
+    TC_DIAG_REG_SEL = 13,
+    TC_DIAG_REG_D_SEL = 14,
+    TC_DIAG_LANE = 15,      // target on a lane qubit
+    TC_DIAG_LANE_SEL = 16,
+    TC_DIAG_UNIFORM = 17,   // target on a warp / outer qubit
+    TC_DIAG_UNIFORM_SEL = 18,
+    TC_DEPHASE = 19,
+    TC_COLLAPSE = 20,
+    TC_DEPOL = 21,      // register bits q0 pos < q1 pos
+    TC_DEPOL_LANE = 22, // t on lane bit q0 pos, t+N on register bit q1 pos
+    TC_LANE_RX = 23,    // Rx-class 2x2 on a lane bit (tolerance mode only: TileParams.fast)
+    TC_LANE_XCHG = 24,  // exchange lane bit q0 pos with register bit q1 pos (pure moves)
+    TC_NUM_CODES = 25,
 };
 
 // Op header packed in one 64-bit word (one constant-bank load per op):
 //   [0,6) TileCode  [6,10) flags  [10] outcome  [11,13) q0 TileLoc
 //   [13,19) q0 pos  [19,21) q1 TileLoc  [21,27) q1 pos  [27,32) lane cmask
-//   [32,36) register cmask  [36,40) warp cmask
+//   [32,37) register cmask  [40,48) unit coefficients (tolerance mode)
+//   [48,52) warp cmask
 struct TileOp {
     uint64_t hdr;
     uint64_t outer_cmask; // controls on qubits outside the tile (global bits)
@@ -196,7 +200,7 @@ QGPU_HD constexpr uint64_t tile_hdr(uint32_t code, uint32_t flags, uint32_t outc
     return uint64_t(code & 63) | uint64_t(flags & 15) << 6 |
            uint64_t(outcome & 1) << 10 | uint64_t(q0k & 3) << 11 | uint64_t(q0p & 63) << 13 |
            uint64_t(q1k & 3) << 19 | uint64_t(q1p & 63) << 21 | uint64_t(lane_cm & 31) << 27 |
-           uint64_t(reg_cm & 15) << 32 | uint64_t(warp_cm & 15) << 36;
+           uint64_t(reg_cm & 31) << 32 | uint64_t(warp_cm & 15) << 48;
 }
 
 // Lane bits 0-2 always span qubits 0-2 (a quarter-warp's 8 lanes read 128

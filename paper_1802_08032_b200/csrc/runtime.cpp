@@ -1002,13 +1002,13 @@ int pass_profile_info(const TileParams& P) {
         double f;
         const uint32_t un = static_cast<uint32_t>((h >> 40) & 0xff);
         auto u = [&](int k) { return (un >> (2 * k)) & 3u; };
-        if (code < TC_REG + 16) { // 2x2 on a register bit, by class row
-            const int row = (code - TC_REG) / 4;
+        if (code < TC_REG + 4) { // 2x2 on a register bit, by class row
+            const int row = code - TC_REG;
             f = row == 0 ? 8.0 : row == 3 ? 0.0 : 4.0;
             if (row == 1 || row == 2) // unit coefficients: one FMA (or add) per component
                 f = ((u(0) || u(1)) ? 1.0 : 2.0) + ((u(2) || u(3)) ? 1.0 : 2.0);
-        } else if (code < TC_REG_SEL + 8) {
-            f = (code - TC_REG_SEL) / 4 == 0 ? 8.0 : 0.0;
+        } else if (code < TC_REG_SEL + 2) {
+            f = code == TC_REG_SEL ? 8.0 : 0.0;
         } else if (code == TC_LANE_GENERIC || code == TC_LANE_SEL_GENERIC) {
             f = 8.0;
         } else if (code == TC_LANE_REAL || code == TC_LANE_RX) {
@@ -1019,8 +1019,7 @@ int pass_profile_info(const TileParams& P) {
             f = 0.0;
         } else if (code == TC_LANE_SWAP || code == TC_LANE_SEL_SWAP) {
             f = 0.0;
-        } else if ((code >= TC_DIAG_REG_D && code < TC_DIAG_REG_D + 4) ||
-                   (code >= TC_DIAG_REG_D_SEL && code < TC_DIAG_REG_D_SEL + 4)) {
+        } else if (code == TC_DIAG_REG_D || code == TC_DIAG_REG_D_SEL) {
             f = 2.0; // only the bit-1 half
         } else if (code == TC_DIAG_UNIFORM || code == TC_DIAG_UNIFORM_SEL) {
             f = (flags & (DF_A_ONE | DF_D_ONE)) ? 2.0 : 4.0;
@@ -1028,7 +1027,7 @@ int pass_profile_info(const TileParams& P) {
             f = 2.0; // symmetric form: two FMAs
         } else if (code == TC_DEPHASE || code == TC_COLLAPSE) {
             f = 2.0;
-        } else if (code >= TC_DEPOL && code < TC_DEPOL_LANE + 4) {
+        } else if (code == TC_DEPOL || code == TC_DEPOL_LANE) {
             f = 3.0;
         } else {
             f = 4.0; // the other diagonals
@@ -1470,13 +1469,12 @@ void QuregImpl::launch_tile() {
             const bool ctrl = lane_cm != 0 || reg_cm != 0 || warp_cm != 0;
             uint32_t code;
             if (op.kind == FK_DEPOL && q0k == TL_LANE && q1k == TL_REG) {
-                code = TC_DEPOL_LANE + q1p;
+                code = TC_DEPOL_LANE;
             } else if (op.kind == FK_DEPOL) {
                 if (q0k != TL_REG || q1k != TL_REG)
                     throw DeviceError("internal: a fused depolarising channel needs register qubits");
-                const int j0 = std::min(q0p, q1p), j1 = std::max(q0p, q1p);
-                static const int pair_index[4][4] = {{-1, 0, 1, 2}, {-1, -1, 3, 4}, {-1, -1, -1, 5}, {-1, -1, -1, -1}};
-                code = TC_DEPOL + pair_index[j0][j1];
+                if (q0p > q1p) std::swap(q0p, q1p); // (symmetric in its two qubits)
+                code = TC_DEPOL;
             } else if (op.kind == FK_DEPHASE) {
                 code = TC_DEPHASE;
             } else if (op.kind == FK_COLLAPSE) {
@@ -1486,8 +1484,8 @@ void QuregImpl::launch_tile() {
                     // a == 1 exactly: the low side is the identity (a * v
                     // with a = 1 + 0i rounds to v), leave it alone
                     const bool d_only = (op.flags & DF_A_ONE) != 0;
-                    code = (ctrl ? (d_only ? TC_DIAG_REG_D_SEL : TC_DIAG_REG_SEL)
-                                 : (d_only ? TC_DIAG_REG_D : TC_DIAG_REG)) + q0p;
+                    code = ctrl ? (d_only ? TC_DIAG_REG_D_SEL : TC_DIAG_REG_SEL)
+                                : (d_only ? TC_DIAG_REG_D : TC_DIAG_REG);
                 } else if (q0k == TL_LANE) {
                     code = ctrl ? TC_DIAG_LANE_SEL : TC_DIAG_LANE;
                 } else {
@@ -1504,9 +1502,9 @@ void QuregImpl::launch_tile() {
             } else { // register bit
                 if (!ctrl) {
                     const uint32_t row = op.cls == CLS_REAL ? 1 : op.cls == CLS_RX ? 2 : op.cls == CLS_SWAP ? 3 : 0;
-                    code = TC_REG + 4 * row + q0p;
+                    code = TC_REG + row;
                 } else {
-                    code = TC_REG_SEL + 4 * (op.cls == CLS_SWAP ? 1 : 0) + q0p;
+                    code = TC_REG_SEL + (op.cls == CLS_SWAP ? 1 : 0);
                 }
             }
             to.hdr = tile_hdr(code, flags, op.outcome, q0k, q0p, q1k, q1p, lane_cm, reg_cm, warp_cm);

@@ -21,6 +21,7 @@ def run(spec: dict, uid: bytes, rank: int, nranks: int, q) -> None:
         out: dict = {"rank": rank}
         try:
             env.set_qubit_swaps(spec["swaps"])
+            env.set_ordering(spec.get("reorder", False))
             if spec.get("chunk"):
                 env.set_exchange_chunk(spec["chunk"])
             n, density = spec["n"], spec["density"]

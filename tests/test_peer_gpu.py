@@ -74,7 +74,10 @@ def check(spec, nranks):
     else:
         want = oracle_run(c, density=density)
     got = np.concatenate([np.frombuffer(outs[r]["shard"], dtype=np.complex128) for r in range(nranks)])
-    assert np.array_equal(got, want), f"max-abs {np.max(np.abs(got - want))}"
+    if spec.get("reorder"):  # commutation-aware schedule: the north star's 1e-12, not bit for bit
+        assert np.max(np.abs(got - want)) <= TOL, f"max-abs {np.max(np.abs(got - want))}"
+    else:
+        assert np.array_equal(got, want), f"max-abs {np.max(np.abs(got - want))}"
     wd = want.astype(np.complex128)
     norm = oracle.orc_trace(wd, n).real if density else oracle.orc_norm_kahan(wd)
     ptol = 1e-6 if single else TOL
@@ -84,7 +87,10 @@ def check(spec, nranks):
             assert abs(o["probs"][t] - oracle.orc_prob_of_outcome(wd, n, t, 1, density)) < ptol
         if o["amp"] is not None:
             i = spec.get("amp_index", 3)
-            assert o["amp"] == (want[i].real, want[i].imag)
+            if spec.get("reorder"):
+                assert abs(complex(*o["amp"]) - want[i]) <= TOL
+            else:
+                assert o["amp"] == (want[i].real, want[i].imag)
     if spec.get("measure"):
         seq = [o["outcomes"] for o in outs.values()]
         assert all(s == seq[0] for s in seq), seq  # the same draw on every rank
@@ -113,6 +119,17 @@ def test_peer_density_matrix_with_channels(nranks, swaps):
     """Depolarising on a qubit whose bra copy is a rank bit runs the peer
     corner-pair kernel (swaps off) or swaps it local (swaps on)."""
     check({"n": 5, "gates": 140, "seed": 70 + nranks, "density": True, "swaps": swaps}, nranks)
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_peer_reordered_tile_passes(nranks):
+    """The library's default schedule on a multi-process register with
+    tile-sized shards (16 qubits, 14-15 local): commutation-aware passes,
+    same-qubit merging and unit coefficients on every rank, qubit swaps
+    moving global targets local — amplitudes, probabilities and measurement
+    within 1e-12 of the oracle, the same outcomes on every rank."""
+    check({"n": 16, "layered": 8, "seed": 12345, "density": False, "swaps": True, "reorder": True,
+           "amp_index": (1 << 16) - 7, "measure": [3, 4], "measure_qubits": [15, 2]}, nranks)
 
 
 def test_peer_layered_circuit_single_precision():

@@ -31,8 +31,7 @@ for rep in range(2):
 
     def stage(name, fn):
         p0, l0, t0 = q.pass_count(), quest.kernel_launches(), time.perf_counter()
-        fn()
-        env.sync()
+        fn()  # (each call returns a value: it completes its own work)
         stages.append((name, (time.perf_counter() - t0) * 1e3, q.pass_count() - p0, quest.kernel_launches() - l0))
 
     stage("prob q0", lambda: q.calcProbOfOutcome(0, 0))
@@ -40,6 +39,9 @@ for rep in range(2):
     for t, o in [(0, 1), (9, 0), (21, 1), (n - 1, 0)]:
         stage(f"collapse {t}", lambda t=t, o=o: q.collapseToOutcome(t, o))
     stage("total", lambda: q.calcTotalProb())
+    t0 = time.perf_counter()
+    env.sync()  # the deferred collapses, applied
+    stages.append(("sync", (time.perf_counter() - t0) * 1e3, 0, 0))
     if rep == 1:
         tot = sum(s[1] for s in stages)
         print(f"tail {tot:.2f} ms")
