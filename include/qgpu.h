@@ -180,6 +180,18 @@ int qgpuPlanPasses(int flatQubits, int numOps, const int* kinds, const int* q0, 
 int qgpuPlanSwaps(int flatQubits, int rankLog2, unsigned long long chunkAmps, int numOps,
                   const int* targets, const int* pairOps, int* swapsOut, int maxSwaps);
 
+/* The distributed schedule alone (host only, no GPU): the ops of
+ * qgpuPlanPasses on logical flat qubits of a register split over
+ * 2^rankLog2 peer-transport ranks, run through the runtime's own queue —
+ * reorder != 0: the light-cone drain (any op that can run with the local
+ * qubits first, swaps only when nothing can) and the reordering window;
+ * 0: circuit order. swapsOut[2i..2i+1] = (global position, local position)
+ * of the i-th swap; *passesOut = tile passes. Returns the number of swaps,
+ * or -1 on invalid input. */
+int qgpuPlanDistributed(int flatQubits, int rankLog2, int numOps, const int* kinds, const int* q0, const int* q1,
+                        const unsigned long long* cmasks, const double* mats, int reorder, int* passesOut,
+                        int* swapsOut, int maxSwaps);
+
 /* Messages / bytes this process's ranks sent for `qureg` (CommStats,
  * distributed.hpp:63-74); arrays of length numRanks (loopback) or 1. */
 void qgpuCommStats(Qureg qureg, unsigned long long* messages, unsigned long long* bytes);

@@ -716,7 +716,7 @@ void initPlusState(Qureg qureg) {
     guarded_void("initPlusState", [&] {
         QuregImpl* r = reg_of(qureg);
         r->discard_all(); // queued logical ops are dead too (lq), not just the open pass
-        r->sp.reset(r->flat, r->local_qubits, r->env->chunk_amps); // uniform state: any layout
+        r->sp.reset(r->flat, r->local_qubits, r->env->swap_granule()); // uniform state: any layout
         const double v = r->density ? 1.0 / static_cast<double>(uint64_t{1} << r->N)
                                     : 1.0 / std::sqrt(static_cast<double>(uint64_t{1} << r->N));
         for (auto& s : r->shards) launch_fill(s.amps, r->single, r->local_len, v, 0.0, r->env->stream);
@@ -777,7 +777,7 @@ void initStateFromAmps(Qureg qureg, qreal* reals, qreal* imags) {
             if (!std::isfinite(reals[i]) || !std::isfinite(imags[i]))
                 throw qgpu::DomainError("amplitude must be finite");
         r->discard_all(); // the whole state is rewritten: drop queued ops and the qubit permutation
-        r->sp.reset(r->flat, r->local_qubits, r->env->chunk_amps);
+        r->sp.reset(r->flat, r->local_qubits, r->env->swap_granule());
         set_amps_impl(r, 0, reals, imags, nullptr, static_cast<long long>(uint64_t{1} << r->flat));
     });
 }
@@ -1336,6 +1336,62 @@ int qgpuPlanPasses(int flatQubits, int numOps, const int* kinds, const int* q0, 
         }
         if (k != numOps) throw qgpu::DeviceError("internal: plan lost ops");
         return static_cast<int>(out.size());
+    });
+}
+
+int qgpuPlanDistributed(int flatQubits, int rankLog2, int numOps, const int* kinds, const int* q0, const int* q1,
+                        const unsigned long long* cmasks, const double* mats, int reorder, int* passesOut,
+                        int* swapsOut, int maxSwaps) {
+    return guarded("qgpuPlanDistributed", -1, [&] {
+        if (rankLog2 < 1 || rankLog2 > 16 || flatQubits - rankLog2 < kTileQubits || flatQubits > 62 || numOps < 0 ||
+            maxSwaps < 0)
+            throw qgpu::DomainError("invalid distributed-plan request");
+        Env e;
+        e.mode = Mode::Peer; // (the swap granule of the peer transport; nothing is launched)
+        e.rank_log2 = rankLog2;
+        e.num_ranks = 1 << rankLog2;
+        e.qubit_swaps = true;
+        e.order = reorder ? 1 : 0;
+        QuregImpl q;
+        q.N = q.flat = flatQubits;
+        q.local_qubits = flatQubits - rankLog2;
+        q.local_len = uint64_t{1} << q.local_qubits;
+        q.env = &e;
+        q.sp.reset(q.flat, q.local_qubits, e.swap_granule());
+        std::vector<QuregImpl::PlannedPass> out;
+        std::vector<std::pair<int, int>> swaps;
+        q.plan_sink = &out;
+        q.swap_sink = &swaps;
+        try {
+            for (int i = 0; i < numOps; ++i) {
+                FlatOp op;
+                op.kind = static_cast<uint8_t>(kinds[i]);
+                op.q0 = q0[i];
+                op.q1 = q1[i];
+                op.cmask = cmasks[i];
+                op.id = i;
+                if (op.q0 < 0 || op.q0 >= flatQubits || op.q1 >= flatQubits || (op.cmask >> flatQubits))
+                    throw qgpu::DomainError("op " + std::to_string(i) + " out of range");
+                if (op.kind == FK_GATE) {
+                    std::memcpy(op.m, mats + 8 * static_cast<size_t>(i), sizeof(op.m));
+                    op.cls = classify(op.m, &op.flags);
+                } else if (op.kind > FK_COLLAPSE) {
+                    throw qgpu::DomainError("op " + std::to_string(i) + ": unknown kind");
+                }
+                q.enqueue(op);
+            }
+            q.flush();
+        } catch (...) {
+            q.env = nullptr;
+            throw;
+        }
+        q.env = nullptr;
+        *passesOut = static_cast<int>(out.size());
+        for (size_t i = 0; i < swaps.size() && static_cast<int>(i) < maxSwaps; ++i) {
+            swapsOut[2 * i] = swaps[i].first;
+            swapsOut[2 * i + 1] = swaps[i].second;
+        }
+        return static_cast<int>(swaps.size());
     });
 }
 

@@ -212,7 +212,7 @@ QuregImpl* create_register(Env* env, int N, bool density, bool single) {
         cudaGetLastError();
         throw ResourceError("failed to allocate reduction scratch");
     }
-    q->sp.reset(flat, q->local_qubits, env->chunk_amps);
+    q->sp.reset(flat, q->local_qubits, env->swap_granule());
     q->fill_zero();
     if (q->shards[0].rank == 0) {
         const double2 one = make_double2(1.0, 0.0);
@@ -246,7 +246,7 @@ void QuregImpl::fill_zero() {
     for (auto& s : shards)
         cuda_check(cudaMemsetAsync(s.amps, 0, local_len * amp_bytes(), env->stream),
                    "cudaMemsetAsync");
-    sp.reset(flat, local_qubits, env->chunk_amps); // the whole state is rewritten
+    sp.reset(flat, local_qubits, env->swap_granule()); // the whole state is rewritten
 }
 
 void QuregImpl::ensure_recv(uint64_t len) {
@@ -814,7 +814,89 @@ void QuregImpl::enqueue(const FlatOp& lop) {
 // channel) must be local, so a global one is swapped in first, evicting the
 // local qubit next needed furthest ahead in the buffered window; diagonal
 // ops, dephasing, collapse and controls work on any position.
+// Light-cone drain (the reordering mode): instead of taking the logical queue
+// in circuit order — a layered circuit touches every qubit once per layer,
+// so the global ones had to be swapped in (and others out) every layer: 34
+// swaps per step of the 36-qubit / 8-rank bench circuit — every op that can
+// run with the current local qubits and commutes with the ops held back
+// before it (op_qubits' rule) is released at once. Only when nothing can run
+// does the first held-back op get its global qubits swapped in, evicting the
+// local qubit needed furthest ahead in the queue: typically one whose work
+// in the queue is done. Dependencies travel one qubit per layer, so the ops
+// far from the global qubits run ahead and the 36-qubit circuit needs about
+// 3-7 swaps per step (host dry run: qgpuPlanSwapsReorder,
+// tests/test_distributed_gloo.py). Results within 1e-12 (commuting ops
+// reordered), like the window scheduler downstream.
+void QuregImpl::drain_lightcone(size_t count) {
+    const size_t target = lq.size() - std::min(count, lq.size()); // ops left queued
+    while (lq.size() > target) {
+        Blockers bl;
+        std::vector<FlatOp> rest;
+        rest.reserve(lq.size());
+        bool any = false;
+        for (const FlatOp& lop : lq) {
+            const OpQubits o = op_qubits(lop);
+            const bool local = (sp.phys_mask(o.need) >> local_qubits) == 0;
+            if (local && !blocked_by(o, bl)) {
+                for (uint64_t m = o.need; m; m &= m - 1) sp.touch(__builtin_ctzll(m));
+                FlatOp op = lop;
+                op.q0 = sp.phys(lop.q0);
+                op.q1 = sp.phys(lop.q1);
+                op.cmask = sp.phys_mask(lop.cmask);
+                enqueue_phys(op);
+                any = true;
+            } else {
+                bl.add(o);
+                rest.push_back(lop);
+            }
+        }
+        lq.swap(rest);
+        if (lq.size() <= target || any) continue;
+        // nothing can run: the first queued op (it has no queued predecessor)
+        // needs a global qubit
+        std::vector<int> need0(lq.size(), -1), need1(lq.size(), -1);
+        for (size_t j = 0; j < lq.size(); ++j) {
+            const FlatOp& o = lq[j];
+            if (o.kind == FK_GATE && o.cls != CLS_DIAG) need0[j] = o.q0;
+            if (o.kind == FK_DEPOL) {
+                need0[j] = o.q0;
+                need1[j] = o.q1;
+            }
+        }
+        const FlatOp& f = lq.front();
+        if (f.kind == FK_GATE && f.cls == CLS_DIAG)
+            throw DeviceError("internal: light-cone drain stuck on an op that needs no local qubit");
+        auto make_local = [&](int logical, uint64_t busy) {
+            const int p = sp.l2p[logical];
+            if (p < local_qubits) return;
+            const int v = sp.victim(busy, need0.data() + 1, need1.data() + 1, lq.size() - 1);
+            // Only the released ops on the two traded positions must run
+            // before the swap; the rest of the pass window commutes with it
+            // (a permutation of other qubits) and stays for fuller passes.
+            const uint64_t moved = (uint64_t{1} << p) | (uint64_t{1} << v);
+            auto pending_on_moved = [&] {
+                for (const FlatOp& w : win) {
+                    const OpQubits o = op_qubits(w);
+                    if ((o.nd | o.nx | o.dg | o.need) & moved) return true;
+                }
+                return false;
+            };
+            while (pending_on_moved()) window_pass();
+            run_swap(p, v, /*flush=*/false);
+            sp.apply(p, v);
+        };
+        uint64_t busy0 = 0;
+        if (need1[0] >= 0 && sp.l2p[need1[0]] < local_qubits) busy0 = uint64_t{1} << sp.l2p[need1[0]];
+        if (need0[0] >= 0) make_local(need0[0], busy0);
+        if (need1[0] >= 0) make_local(need1[0], uint64_t{1} << sp.l2p[need0[0]]);
+    }
+}
+
 void QuregImpl::drain(size_t count) {
+    if (reorder_on()) {
+        drain_lightcone(count);
+        return;
+    }
     count = std::min(count, lq.size());
     std::vector<int> need0(lq.size(), -1), need1(lq.size(), -1);
     for (size_t j = 0; j < lq.size(); ++j) {
@@ -1815,8 +1897,19 @@ void QuregImpl::run_depol(const FlatOp& op) {
 // and receive the same local offsets (a pure copy, in sub-chunks of
 // min(chunk, 2^v) contiguous amplitudes, double-buffered like the exchange
 // gates).
-void QuregImpl::run_swap(int g, int v) {
-    flush_pass(); // queued ops (e.g. restore_identity's local swaps) run first
+void QuregImpl::run_swap(int g, int v, bool flush) {
+    // queued ops (e.g. restore_identity's local swaps) run first; the
+    // light-cone drain has already run the ones on the traded positions
+    if (flush) {
+        flush_pass();
+    } else if (!pending.empty()) { // (the open pass; the window stays)
+        launch_tile();
+        discard();
+    }
+    if (swap_sink) { // dry run (qgpuPlanDistributed)
+        swap_sink->push_back({g, v});
+        return;
+    }
     const int j = g - local_qubits;
     const uint64_t block = uint64_t{1} << v;
     const uint64_t unit = std::min<uint64_t>(std::min<uint64_t>(env->chunk_amps, block), local_len / 2);

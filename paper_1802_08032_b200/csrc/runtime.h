@@ -90,6 +90,13 @@ struct Env {
     std::unique_ptr<NcclComm> nccl;
     std::unique_ptr<PeerGroup> peer;
     bool multi_process() const { return mode == Mode::Nccl || mode == Mode::Peer; }
+    // smallest contiguous block a global<->local swap should trade (swap
+    // victims sit at positions >= its log2): the sub-chunk of the send /
+    // receive transports; the peer kernel moves blocks of 2^5 amplitudes
+    // (coalesced warps), which keeps victims off the lane qubits 0-4 (a
+    // global qubit landing there would make its gates shuffle ops) while
+    // the light-cone drain can evict the low qubits whose work is done
+    uint64_t swap_granule() const { return mode == Mode::Peer ? 32 : chunk_amps; }
     std::set<struct QuregImpl*> quregs;
 
     // Launch profiling (qgpuProfileStart/Stop): an event pair around every
@@ -213,6 +220,7 @@ struct QuregImpl {
         std::vector<int> phase_begin; // index into ids where each phase starts
     };
     std::vector<PlannedPass>* plan_sink = nullptr;
+    std::vector<std::pair<int, int>>* swap_sink = nullptr; // dry runs: (global, local) swaps
 
     // logical -> physical qubit map (global<->local swaps, swap_plan.h)
     SwapPlanner sp;
@@ -225,6 +233,7 @@ struct QuregImpl {
     void enqueue_phys(const FlatOp& op);
     std::vector<FlatOp> lq;       // logical ops awaiting swap planning
     void drain(size_t count);     // plan + enqueue_phys the first `count` of lq
+    void drain_lightcone(size_t count); // (reordering mode: any runnable ops first)
     void flush_pass();            // launch the open pass
     bool swaps_on() const { return env->qubit_swaps && env->rank_log2 > 0; }
     // move every logical qubit back to its own position (before amplitudes
@@ -289,7 +298,9 @@ struct QuregImpl {
     void launch_fused();
     void run_exchange_gate(const FlatOp& op);
     void run_depol(const FlatOp& op);
-    void run_swap(int g, int v); // trade physical global position g with local v
+    // trade physical global position g with local v; flush = false: only the
+    // open pass runs first (the caller ran the window's ops on g and v)
+    void run_swap(int g, int v, bool flush = true);
     void local_swap(int a, int b);
     void ensure_recv(uint64_t len);
     uint64_t goff(const Shard& s) const { return static_cast<uint64_t>(s.rank) * local_len; }

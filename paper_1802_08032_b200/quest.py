@@ -164,6 +164,7 @@ _SIGS = {
     "qgpuGetOrdering": (_I, [QuESTEnv]),
     "qgpuPlanPasses": (_I, [_I, _I, _VP, _VP, _VP, _VP, _VP, _I, _I, _I, _VP, _VP, _VP]),
     "qgpuPlanSwaps": (_I, [_I, _I, _ULL, _I, _VP, _VP, _VP, _I]),
+    "qgpuPlanDistributed": (_I, [_I, _I, _I, _VP, _VP, _VP, _VP, _VP, _I, _VP, _VP, _I]),
     "qgpuCommStats": (None, [Qureg, _VP, _VP]),
     "qgpuPlanGate": (_I, [_I, _I, _I, _I, _ULL, _IP, _IP, ctypes.POINTER(ctypes.c_ulonglong)]),
     "qgpuPlanChunks": (_I, [_ULL, _ULL, ctypes.POINTER(ctypes.c_ulonglong)]),
@@ -511,6 +512,32 @@ def plan_swaps(flat: int, rank_log2: int, ops, chunk_amps: int = 1 << 24):
     if n < 0:
         check()
     return [tuple(int(x) for x in out[3 * i:3 * i + 3]) for i in range(n)]
+
+
+def plan_distributed(flat: int, rank_log2: int, ops, reorder: bool = True):
+    """qgpuPlanDistributed (host only): ops as for plan_passes, on logical
+    qubits of a register over 2^rank_log2 ranks. Returns (passes, [(global
+    position, local position) per swap])."""
+    import numpy as np
+
+    n = len(ops)
+    kinds = np.array([o[0] for o in ops], dtype=np.int32)
+    q0 = np.array([o[1] for o in ops], dtype=np.int32)
+    q1 = np.array([o[2] for o in ops], dtype=np.int32)
+    cm = np.array([o[3] for o in ops], dtype=np.uint64)
+    mats = np.zeros((max(1, n), 8), dtype=np.float64)
+    for i, o in enumerate(ops):
+        if o[0] == 0:
+            mats[i] = o[4]
+    passes = np.zeros(1, dtype=np.int32)
+    cap = 4 * max(1, n)
+    sw = np.zeros(2 * cap, dtype=np.int32)
+    r = lib().qgpuPlanDistributed(flat, rank_log2, n, kinds.ctypes.data, q0.ctypes.data, q1.ctypes.data,
+                                  cm.ctypes.data, mats.ctypes.data, int(reorder), passes.ctypes.data,
+                                  sw.ctypes.data, cap)
+    if r < 0:
+        check()
+    return int(passes[0]), [(int(sw[2 * i]), int(sw[2 * i + 1])) for i in range(min(r, cap))]
 
 
 def plan_passes(flat: int, ops, reorder: bool = True, window: int = 0, max_phases: int = 3):

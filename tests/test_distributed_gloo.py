@@ -165,3 +165,24 @@ def test_swap_plan_traffic_on_layered_circuits():
         assert 0.5 * len(plan) < 0.45 * exch, (n, k, len(plan), exch)
         # every swap trades a global position for a local one
         assert all(g >= n - k > v for _, g, v in plan)
+
+
+def test_lightcone_drain_swaps_on_layered_circuits():
+    """The default ordering's light-cone drain (qgpuPlanDistributed, host
+    dry run of the runtime's own queue): a layered circuit touches every
+    qubit per layer, so circuit order swaps the global qubits in and out
+    every few layers; releasing every op that can run with the local qubits
+    first needs a handful of swaps per step — and far fewer tile passes,
+    since each swap drains the pass window. 36 qubits on 8 ranks (BASELINE
+    C3b): 6 swaps and 34 passes per step against 27 and 97."""
+    from paper_1802_08032_b200 import circuits as C
+    from tests.test_reorder_plan import flat_ops
+
+    for n, k, max_swaps in [(36, 3, 8), (35, 2, 6), (34, 1, 3), (27, 1, 3)]:
+        ops = flat_ops(C.layered_random_circuit(n, 20, 12345))
+        p_lc, sw_lc = quest.plan_distributed(n, k, ops, reorder=True)
+        p_ex, sw_ex = quest.plan_distributed(n, k, ops, reorder=False)
+        assert len(sw_lc) <= max_swaps, (n, k, len(sw_lc))
+        assert 2 * len(sw_lc) < len(sw_ex) and 2 * p_lc < p_ex, (n, k, p_lc, p_ex, len(sw_lc), len(sw_ex))
+        # every swap trades a global position for a local one off the lane qubits
+        assert all(g >= n - k and 5 <= v < n - k for g, v in sw_lc)

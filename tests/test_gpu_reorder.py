@@ -153,6 +153,38 @@ def test_loopback_ranks(k, swaps):
         e.destroy()
 
 
+@pytest.mark.parametrize("k", [1, 3])
+def test_loopback_lightcone_drain(k):
+    """Qubit swaps in the default ordering go through the light-cone drain
+    (runtime.cpp drain_lightcone: ops that can run with the local qubits go
+    first, global qubits are swapped in only when nothing can): a layered
+    circuit (every qubit touched per layer) and a noisy density matrix
+    (depolarising needs both of its qubits local) on 2^k virtual ranks,
+    within 1e-12 of the oracle (the swap counts: tests/test_distributed_gloo.py)."""
+    n = 17
+    c = C.layered_random_circuit(n, 12, 12345)
+    want = oracle_run(c)
+    e = make_env(loopback=1 << k)
+    try:
+        e.set_qubit_swaps(True)
+        q = quest.QuregHandle(e, n)
+        try:
+            C.apply_circuit(q, c)
+            assert max_err(q.state(), want) <= TOL
+        finally:
+            q.destroy()
+        d = C.layered_random_circuit(7, 4, 8, noise_pmax=0.1)
+        dw = oracle_run(d, density=True)
+        qd = quest.QuregHandle(e, 7, True)
+        try:
+            C.apply_circuit(qd, d)
+            assert max_err(qd.state(), dw) <= TOL
+        finally:
+            qd.destroy()
+    finally:
+        e.destroy()
+
+
 def test_measurement_and_collapse(env):
     n = 16
     c = random_gate_circuit(n, 200, seed=77, max_controls=2)
