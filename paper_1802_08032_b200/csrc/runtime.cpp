@@ -869,7 +869,12 @@ void QuregImpl::drain_lightcone(size_t count) {
         auto make_local = [&](int logical, uint64_t busy) {
             const int p = sp.l2p[logical];
             if (p < local_qubits) return;
-            const int v = sp.victim(busy, need0.data() + 1, need1.data() + 1, lq.size() - 1);
+            uint64_t in_window = 0; // positions the pass window still acts on
+            for (const FlatOp& w : win) {
+                const OpQubits o = op_qubits(w);
+                in_window |= o.nd | o.nx | o.dg | o.need;
+            }
+            const int v = sp.victim(busy, need0.data() + 1, need1.data() + 1, lq.size() - 1, in_window);
             // Only the released ops on the two traded positions must run
             // before the swap; the rest of the pass window commutes with it
             // (a permutation of other qubits) and stays for fuller passes.

@@ -31,7 +31,7 @@ bool SwapPlanner::identity() const {
     return true;
 }
 
-int SwapPlanner::victim(uint64_t busy, const int* need0, const int* need1, size_t nfuture) const {
+int SwapPlanner::victim(uint64_t busy, const int* need0, const int* need1, size_t nfuture, uint64_t pending) const {
     // distance to each logical qubit's next local use in the window
     std::vector<size_t> next(flat, ~size_t{0});
     for (size_t j = nfuture; j-- > 0;) {
@@ -40,15 +40,19 @@ int SwapPlanner::victim(uint64_t busy, const int* need0, const int* need1, size_
     }
     int best = -1;
     size_t best_next = 0;
+    bool best_pend = false;
     uint64_t best_use = 0;
     for (int v = local - 1; v >= min_victim; --v) {
         if ((busy >> v) & 1) continue;
         const int L = p2l[v];
         const size_t nx = next[L];
+        const bool pend = (pending >> v) & 1;
         const uint64_t u = last_use[L];
-        if (best < 0 || nx > best_next || (nx == best_next && u < best_use)) {
+        if (best < 0 || nx > best_next || (nx == best_next && best_pend && !pend) ||
+            (nx == best_next && pend == best_pend && u < best_use)) {
             best = v;
             best_next = nx;
+            best_pend = pend;
             best_use = u;
         }
     }

@@ -42,8 +42,11 @@ struct SwapPlanner {
     // local physical position to trade for a global one; `busy` = physical
     // positions the current op needs local (never evicted); need0/need1[j] =
     // logical qubits future op j needs local (-1: none), j < nfuture
+    // `pending` = physical positions with ops still waiting in the pass
+    // window (a victim among those forces them to run first): preferred
+    // against on equal lookahead distance
     int victim(uint64_t busy, const int* need0 = nullptr, const int* need1 = nullptr,
-               size_t nfuture = 0) const;
+               size_t nfuture = 0, uint64_t pending = 0) const;
     // swap the logical qubits at physical positions a and b
     void apply(int a, int b);
     int phys(int logical) const { return logical < 0 ? logical : l2p[logical]; }
