@@ -39,6 +39,9 @@ void jit_wait();              // block until every queued compile finished
 void jit_set_mode(int mode);  // 0 off, 1 background compiles, 2 compile before first use
 int jit_mode();
 void jit_shutdown();
+// writes pass k's generated program (both coefficient variants) to
+// dir/pass_<k>.cu and dir/pass_<k>_smem.cu (dry runs, offline inspection)
+void jit_dump_program(const TileParams& P, const char* dir, int k);
 void jit_stats(unsigned long long* kernels, unsigned long long* failed, unsigned long long* pending);
 int jit_selftest(char* log, int len, double* seconds); // host only: cubin bytes or -1
 

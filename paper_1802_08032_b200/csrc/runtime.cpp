@@ -1140,8 +1140,14 @@ void QuregImpl::launch_tile() {
         at[pending.size()] = static_cast<int>(pp.ids.size());
         for (const PhaseState& ph : phases) pp.phase_begin.push_back(at[ph.op_begin]);
         plan_sink->push_back(std::move(pp));
-        ++passes;
-        return;
+        // QGPU_PLAN_JIT_DUMP=<dir>: dry runs also build the pass parameters
+        // and write each pass's generated JIT program there (offline SASS
+        // inspection: tools/jit_offline.py)
+        static const char* dump_dir = std::getenv("QGPU_PLAN_JIT_DUMP");
+        if (!dump_dir) {
+            ++passes;
+            return;
+        }
     }
     // The tile's high qubits: the pass's pair targets, topped up with the
     // lowest unused local qubits (qubits 5, 6, 7 let a warp's last-phase
@@ -1621,6 +1627,11 @@ void QuregImpl::launch_tile() {
     P.skip_ones = common & local_mask;
     const uint64_t rank_need = common & ~local_mask;
     P.num_tiles >>= __builtin_popcountll(P.skip_ones);
+    if (plan_sink) { // (dry run with QGPU_PLAN_JIT_DUMP)
+        jit_dump_program(P, std::getenv("QGPU_PLAN_JIT_DUMP"), static_cast<int>(passes));
+        ++passes;
+        return;
+    }
     if (pass_stats_enabled()) record_pass_stats(P);
     ProfScope prof(env, PK_PASS, pass_profile_info(P));
     for (auto& s : shards) {
