@@ -1352,6 +1352,7 @@ int qgpuPlanDistributed(int flatQubits, int rankLog2, int numOps, const int* kin
         e.num_ranks = 1 << rankLog2;
         e.qubit_swaps = true;
         e.order = reorder ? 1 : 0;
+        e.tile_phases = 3; // as on the GPU with the per-pass JIT (the host has no driver to JIT with)
         QuregImpl q;
         q.N = q.flat = flatQubits;
         q.local_qubits = flatQubits - rankLog2;

@@ -174,7 +174,7 @@ def test_lightcone_drain_swaps_on_layered_circuits():
     every few layers; releasing every op that can run with the local qubits
     first needs a handful of swaps per step — and far fewer tile passes,
     since each swap drains the pass window. 36 qubits on 8 ranks (BASELINE
-    C3b): 6 swaps and 34 passes per step against 27 and 97."""
+    C3b): 6 swaps and 25 passes per step against 27 and 96."""
     from paper_1802_08032_b200 import circuits as C
     from tests.test_reorder_plan import flat_ops
 
