@@ -69,6 +69,39 @@ __global__ void k_shfl_idx(float* out, int iters) {
     out[blockIdx.x * blockDim.x + threadIdx.x] = a + b + c + d;
 }
 
+// SHFL and LDS.128 interleaved, independent: do shuffles and shared-memory
+// loads share one pipe (time ~ their sum) or overlap (~ the max)?
+__global__ void k_shfl_lds(double2* out, int iters) {
+    __shared__ double2 s[2048];
+    for (int i = threadIdx.x; i < 2048; i += blockDim.x) s[i] = make_double2(i, i);
+    __syncthreads();
+    float a = threadIdx.x, b = a + 1, c = a + 2, d = a + 3;
+    double2 acc = make_double2(0, 0);
+    unsigned idx = threadIdx.x;
+    for (int i = 0; i < iters; ++i) {
+        double2 x0 = s[(idx) & 2047], x1 = s[(idx + 256) & 2047], x2 = s[(idx + 512) & 2047], x3 = s[(idx + 768) & 2047];
+        a = __shfl_xor_sync(0xffffffffu, a, 1);
+        b = __shfl_xor_sync(0xffffffffu, b, 2);
+        c = __shfl_xor_sync(0xffffffffu, c, 4);
+        d = __shfl_xor_sync(0xffffffffu, d, 8);
+        a = __shfl_xor_sync(0xffffffffu, a, 16);
+        b = __shfl_xor_sync(0xffffffffu, b, 1);
+        c = __shfl_xor_sync(0xffffffffu, c, 2);
+        d = __shfl_xor_sync(0xffffffffu, d, 4);
+        a = __shfl_xor_sync(0xffffffffu, a, 8);
+        b = __shfl_xor_sync(0xffffffffu, b, 16);
+        c = __shfl_xor_sync(0xffffffffu, c, 1);
+        d = __shfl_xor_sync(0xffffffffu, d, 2);
+        a = __shfl_xor_sync(0xffffffffu, a, 4);
+        b = __shfl_xor_sync(0xffffffffu, b, 8);
+        c = __shfl_xor_sync(0xffffffffu, c, 16);
+        d = __shfl_xor_sync(0xffffffffu, d, 1);
+        acc.x += x0.x + x1.x + x2.x + x3.x;
+        idx += 32;
+    }
+    out[blockIdx.x * blockDim.x + threadIdx.x] = make_double2(acc.x + a + b + c + d, 0);
+}
+
 template <class K, class T>
 void run(const char* name, K kern, T* buf, int iters, double instr_per_iter_per_warp, int threads) {
     cudaEvent_t a, b;
@@ -97,5 +130,8 @@ int main() {
     run("LDS.128", k_lds, (double2*)buf, 20000, 4, 256);
     run("SHFL.IDX", k_shfl_idx, (float*)buf, 20000, 4, 512);
     run("MIX", k_mix, (double*)buf, 20000, 12, 512); // 4 SHFL + 8 DFMA per iteration
+    // 4 LDS.128 (16 shared cycles) + 16 SHFL per iteration: ~16 cycles if
+    // they overlap, ~32 if they share the pipe (warp-instructions counted: 20)
+    run("SHFL+LDS", k_shfl_lds, (double2*)buf, 20000, 20, 256);
     return 0;
 }
