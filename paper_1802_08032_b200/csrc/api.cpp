@@ -340,6 +340,7 @@ QuESTEnv make_env(Mode mode, int rank, int nranks, int device, const char* id128
     if (const char* v = std::getenv("QGPU_NORMALIZE")) e->normalize = std::atoi(v); // (2: no symmetric lane diagonals)
     if (const char* v = std::getenv("QGPU_XCHG")) e->exchanges = std::atoi(v);
     if (const char* v = std::getenv("QGPU_MERGE")) e->merge = std::atoi(v) != 0;
+    if (const char* v = std::getenv("QGPU_SWIZZLE")) e->swizzle = std::max(0, std::atoi(v));
     if (const char* v = std::getenv("QGPU_TILE_PHASES"))
         e->tile_phases = std::clamp(std::atoi(v), 1, qgpu::kMaxPhases);
     if (mode == Mode::Nccl && nranks > 1) e->nccl = std::make_unique<NcclComm>(rank, nranks, id128);
@@ -1286,6 +1287,7 @@ int qgpuPlanPasses(int flatQubits, int numOps, const int* kinds, const int* q0, 
         if (const char* v = std::getenv("QGPU_LANE_CAP")) e.lane_cap = std::max(0, std::atoi(v));
         if (const char* v = std::getenv("QGPU_XCHG")) e.exchanges = std::atoi(v);
         if (const char* v = std::getenv("QGPU_MERGE")) e.merge = std::atoi(v) != 0;
+        if (const char* v = std::getenv("QGPU_SWIZZLE")) e.swizzle = std::max(0, std::atoi(v));
         e.order = reorder ? 1 : 0;
         if (windowOps > 0) e.window = windowOps;
         e.tile_phases = maxPhases;

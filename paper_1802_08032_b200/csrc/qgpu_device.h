@@ -219,6 +219,15 @@ struct TilePhase {
     // on named barriers bar_base + group (each transition its own IDs)
     uint16_t sync_bits;
     uint16_t bar_base;
+    // Swizzled layouts (runtime.cpp: a middle phase holding qubits 0-2 in
+    // registers). swz != 0: shared-memory positions are XORs of per-part
+    // offsets — reading: reg_off[i] ^ warp_off[w] ^ lane_in[lane bits];
+    // writing: reg_out[i] ^ warp_out[w] ^ lane_out[lane bits] — instead of
+    // sums with lane bits 0-2 on tile bits 0-2.
+    uint16_t swz;
+    uint16_t lane_in[5], lane_out[5];
+    uint16_t reg_out[1 << kPhaseRegBits];
+    uint16_t warp_out[1 << kTileWarpBits];
 };
 
 struct TileParams {

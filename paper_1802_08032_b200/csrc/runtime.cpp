@@ -681,11 +681,30 @@ void QuregImpl::window_pass() {
         if (op.q0 < lf) return true;
         return !in(R, op.q0) && static_cast<int>(R.size()) >= kPhaseRegBits; // 3, 4 as lane bits
     };
+    // Swizzled middle phase (Env::swizzle): when the pass has enough pair ops
+    // on the fixed lane qubits 0-2, the first phase holds them back and the
+    // second holds qubits 0-2 as register qubits (its lanes 0-2 span three
+    // other tile qubits; the shared-memory layouts around it are XOR-swizzled
+    // so every access stays conflict-free), so they run without shuffles.
+    auto fixed_pair = [&](size_t j) {
+        const FlatOp& op = win[j];
+        return op.kind == FK_GATE && op.cls != CLS_DIAG && op.q0 < lf;
+    };
+    bool plan_mid = false;
+    if (env->swizzle > 0 && !single && lf == kFixedLaneBits && maxph >= 3) {
+        int n = 0;
+        for (size_t j = 0; j < W; ++j) n += sel[j] && fixed_pair(j);
+        plan_mid = n >= env->swizzle;
+    }
     std::vector<size_t> pwin; // window index of each pending op
     while (static_cast<int>(phases.size()) < maxph && pending.size() < cap) {
         PhaseState ph;
         ph.op_begin = static_cast<int>(pending.size());
         std::vector<int>& R = ph.regs;
+        const bool hold = plan_mid && phases.empty(); // (fixed-lane pair ops wait for the middle phase)
+        ph.mid = plan_mid && phases.size() == 1;
+        if (ph.mid)
+            for (int q = 0; q < kFixedLaneBits; ++q) R.push_back(q);
         bool any = false;
         for (;;) {
             bool progress = true;
@@ -695,9 +714,9 @@ void QuregImpl::window_pass() {
                 for (size_t j = 0; j < W; ++j) {
                     if (!sel[j] || taken[j]) continue;
                     int qs[2];
-                    const bool lane = shuffles(j, R);
+                    const bool lane = !ph.mid && shuffles(j, R);
                     if (pending.size() < cap && !blocked_by(oq[j], bl) && missing(j, R, qs) == 0 &&
-                        !(lane && env->lane_cap > 0 && lane_ops >= env->lane_cap)) {
+                        !(hold && fixed_pair(j)) && !(lane && env->lane_cap > 0 && lane_ops >= env->lane_cap)) {
                         const FlatOp& op = win[j];
                         if (lane) ++lane_ops;
                         // qubits 3, 4: a register qubit while the phase has
@@ -739,12 +758,17 @@ void QuregImpl::window_pass() {
         phases.push_back(ph);
     }
     if (pending.empty()) throw DeviceError("internal: reorder scheduler formed an empty pass");
+    if (!phases.empty() && phases.back().mid) { // a middle phase must not be last: an empty standard one follows
+        PhaseState tail;
+        tail.op_begin = static_cast<int>(pending.size());
+        phases.push_back(tail);
+    }
     // Room for the lane <-> register exchanges launch_tile adds (two per lane
     // qubit with two or more pair ops in a phase, at most one per register
     // bit): the pass's last ops go back to the window if needed (a suffix of
     // a dependency-ordered list: nothing kept depends on them).
     auto xneed = [&]() {
-        if (env->exchanges != 1) return 0; // (2: exchanges only where a pass has room)
+        if (env->exchanges != 1 || plan_mid) return 0; // (2: exchanges only where a pass has room)
         int need = 0;
         for (size_t p = 0; p < phases.size(); ++p) {
             const size_t b = static_cast<size_t>(phases[p].op_begin);
@@ -1194,7 +1218,7 @@ void QuregImpl::launch_tile() {
     // 2^(WB - c) warps, which synchronise on a named barrier instead of the
     // whole CTA (c = shared bits; kernel: TilePhase.sync_bits).
     const size_t nph = phases.size();
-    std::vector<std::vector<int>> RB(nph), LB(nph), WBv(nph);
+    std::vector<std::vector<int>> RB(nph), LB(nph), WBv(nph), KB(nph); // KB: a middle phase's lanes 0-2
     auto has = [](const std::vector<int>& v, int t) { return std::find(v.begin(), v.end(), t) != v.end(); };
     for (size_t p = 0; p < nph; ++p)
         for (int q : phases[p].regs) RB[p].push_back(tbit(q));
@@ -1233,13 +1257,16 @@ void QuregImpl::launch_tile() {
                     !has(LB[p], op.q0))
                     LB[p].push_back(op.q0);
             }
-            for (int t : pref)
-                if (LB[p].size() < 2 && !has(RB[p], t) && !has(LB[p], t)) LB[p].push_back(t);
+            for (int t : pref) // (a middle phase's registers include tile bits 0-2: never lane bits 3-4)
+                if (LB[p].size() < 2 && t >= kFixedLaneBits && !has(RB[p], t) && !has(LB[p], t)) LB[p].push_back(t);
             for (int t = kFixedLaneBits; t < kTileQubits && LB[p].size() < 2; ++t)
                 if (!has(RB[p], t) && !has(LB[p], t)) LB[p].push_back(t);
         }
+        if (phases[p].mid) // lanes 0-2: three other tile bits (qubits 0-2 are registers here)
+            for (int t = kTileQubits - 1; t >= kFixedLaneBits && KB[p].size() < 3; --t)
+                if (!has(RB[p], t) && !has(LB[p], t)) KB[p].push_back(t);
         for (int t = kFixedLaneBits; t < kTileQubits; ++t)
-            if (!has(RB[p], t) && !has(LB[p], t)) WBv[p].push_back(t);
+            if (!has(RB[p], t) && !has(LB[p], t) && !has(KB[p], t)) WBv[p].push_back(t);
     }
     // order warp bits: bits shared with the next phase on top (same order)
     std::vector<int> sync_bits(nph, 0);
@@ -1321,7 +1348,7 @@ void QuregImpl::launch_tile() {
         }
         high = nh;
         for (size_t p = 0; p < nph; ++p)
-            for (auto* v : {&RB[p], &LB[p], &WBv[p]})
+            for (auto* v : {&RB[p], &LB[p], &WBv[p], &KB[p]})
                 for (int& t : *v) t = remap[t];
         for (int j = 0; j < kTileHigh; ++j) P.high_pos[j] = high[j];
         {
@@ -1416,6 +1443,24 @@ void QuregImpl::launch_tile() {
         }
         return seq;
     };
+    // Swizzled passes (a middle phase, PhaseState::mid): the shared-memory
+    // position of tile index x in the buffers written by the first and the
+    // middle phase is x ^ spread(x), spread() moving the middle phase's lane
+    // tile bits K[0..2] to bits 0-2. A quarter-warp then hits 8 distinct
+    // 16-byte bank groups both where its lanes span tile bits 0-2 (the first
+    // and last phases) and where they span K (the middle phase); the TMA fill
+    // read by the first phase stays linear. Positions are linear in x, so
+    // each phase's per-part offsets combine by XOR (TilePhase.swz).
+    std::vector<int> key;
+    for (size_t p = 0; p < nph; ++p)
+        if (phases[p].mid) key = KB[p];
+    const bool swz = !key.empty();
+    auto pos = [&](uint32_t x, bool keyed) {
+        if (!keyed) return x;
+        uint32_t sp3 = 0;
+        for (int j = 0; j < 3; ++j) sp3 |= ((x >> key[j]) & 1u) << j;
+        return x ^ sp3;
+    };
     int ko = 0, xchg_used = 0; // emitted ops, exchanges among them
     for (size_t p = 0; p < phases.size(); ++p) {
         TilePhase& Q = P.phases[p];
@@ -1424,19 +1469,41 @@ void QuregImpl::launch_tile() {
         const std::vector<int>& wb = WBv[p];
         Q.sync_bits = static_cast<uint16_t>(sync_bits[p]);
         Q.bar_base = static_cast<uint16_t>(bar_base[p]);
+        const bool in_keyed = swz && p > 0, out_keyed = swz && p + 1 < nph;
         for (int i = 0; i < (1 << kPhaseRegBits); ++i) {
             uint32_t off = 0;
             for (int j = 0; j < kPhaseRegBits; ++j)
                 if ((i >> j) & 1) off |= 1u << rb[j];
-            Q.reg_off[i] = static_cast<uint16_t>(off);
+            Q.reg_off[i] = static_cast<uint16_t>(pos(off, in_keyed));
+            Q.reg_out[i] = static_cast<uint16_t>(pos(off, out_keyed));
         }
         for (int w = 0; w < (1 << kTileWarpBits); ++w) {
             uint32_t off = 0;
             for (int j = 0; j < kTileWarpBits; ++j)
                 if ((w >> j) & 1) off |= 1u << wb[j];
-            Q.warp_off[w] = static_cast<uint16_t>(off);
+            Q.warp_off[w] = static_cast<uint16_t>(pos(off, in_keyed));
+            Q.warp_out[w] = static_cast<uint16_t>(pos(off, out_keyed));
         }
         for (int j = 0; j < 2; ++j) Q.lane_off[j] = static_cast<uint16_t>(1u << lb[j]);
+        // tile bits on lane bits 0-4
+        const int lt[kLaneQubits] = {phases[p].mid ? KB[p][0] : 0, phases[p].mid ? KB[p][1] : 1,
+                                     phases[p].mid ? KB[p][2] : 2, lb[0], lb[1]};
+        Q.swz = swz ? 1 : 0;
+        { // every tile bit exactly once on a lane, register or warp bit of this phase
+            uint32_t seen = 0;
+            auto claim = [&](int t) {
+                if (t < 0 || t >= kTileQubits || ((seen >> t) & 1u))
+                    throw DeviceError("internal: tile layout maps a tile bit twice");
+                seen |= 1u << t;
+            };
+            for (int t : lt) claim(t);
+            for (int j = 0; j < kPhaseRegBits; ++j) claim(rb[j]);
+            for (int j = 0; j < kTileWarpBits; ++j) claim(wb[j]);
+        }
+        for (int j = 0; j < kLaneQubits; ++j) {
+            Q.lane_in[j] = static_cast<uint16_t>(pos(1u << lt[j], in_keyed));
+            Q.lane_out[j] = static_cast<uint16_t>(pos(1u << lt[j], out_keyed));
+        }
         auto gbit = [&](int t) -> uint64_t {
             return t < kLaneQubits ? uint64_t{1} << t : uint64_t{1} << high[t - kLaneQubits];
         };
@@ -1496,10 +1563,10 @@ void QuregImpl::launch_tile() {
         // and register bits, updated by lane <-> register exchanges
         // (plan_exchanges: a run of pair ops on a lane qubit runs on a
         // register bit between two exchanges instead of as shuffle ops).
-        int cur_lane[kLaneQubits] = {0, 1, 2, lb[0], lb[1]};
+        int cur_lane[kLaneQubits] = {lt[0], lt[1], lt[2], lt[3], lt[4]};
         int cur_reg[kPhaseRegBits];
         for (int j = 0; j < kPhaseRegBits; ++j) cur_reg[j] = rb[j];
-        const int xroom = kMaxTileOps - static_cast<int>(pending.size()) - xchg_used;
+        const int xroom = swz ? 0 : kMaxTileOps - static_cast<int>(pending.size()) - xchg_used;
         const std::vector<int> seq = plan_exchanges(begin, end, cur_lane, cur_reg, xroom);
         Q.op_begin = static_cast<uint16_t>(ko);
         auto loc = [&](int q, uint8_t* kind, uint8_t* pos) {
@@ -1612,8 +1679,7 @@ void QuregImpl::launch_tile() {
             std::memcpy(to.m, op.m, sizeof(to.m));
         }
         for (int j = 0; j < kLaneQubits; ++j)
-            if (cur_lane[j] != (j < kFixedLaneBits ? j : lb[j - kFixedLaneBits]))
-                throw DeviceError("internal: a lane exchange was not undone within its phase");
+            if (cur_lane[j] != lt[j]) throw DeviceError("internal: a lane exchange was not undone within its phase");
         Q.op_end = static_cast<uint16_t>(ko);
     }
     // Bits every op needs at 1 outside the tile: local ones shrink the tile

@@ -87,6 +87,11 @@ struct Env {
     // measured slower on the bench circuit, the per-element selects of an
     // exchange cost more ALU issue than the shuffles they save)
     int exchanges = 0;
+    // swizzled middle phases (QGPU_SWIZZLE=<n>): a reordered pass with at
+    // least n pair ops on qubits 0-2 gets a middle phase holding them as
+    // register qubits (tile_body.inc: TilePhase.swz); 0 = off. 30q bench:
+    // 154.1 ms per step at n = 6, 155.7 at 3, 164.8 off (profiles/r2/r2sw)
+    int swizzle = 6;
     std::unique_ptr<NcclComm> nccl;
     std::unique_ptr<PeerGroup> peer;
     bool multi_process() const { return mode == Mode::Nccl || mode == Mode::Peer; }
@@ -194,6 +199,7 @@ struct QuregImpl {
     struct PhaseState {
         std::vector<int> regs; // register qubits of the phase
         int op_begin = 0;
+        bool mid = false; // swizzled middle phase: qubits 0-2 are register qubits
     };
     std::vector<int> tile_high;      // tile pass: high qubits in the tile
     std::vector<PhaseState> phases;  // tile pass: phases
