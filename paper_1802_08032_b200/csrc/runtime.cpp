@@ -697,11 +697,20 @@ void QuregImpl::window_pass() {
         plan_mid = n >= env->swizzle;
     }
     std::vector<size_t> pwin; // window index of each pending op
+    for (int attempt = 0;; ++attempt) {
     while (static_cast<int>(phases.size()) < maxph && pending.size() < cap) {
         PhaseState ph;
         ph.op_begin = static_cast<int>(pending.size());
         std::vector<int>& R = ph.regs;
-        const bool hold = plan_mid && phases.empty(); // (fixed-lane pair ops wait for the middle phase)
+        // (fixed-lane pair ops wait for the middle phase, and after it for
+        // the next pass's one rather than shuffling in the last phase:
+        // 156.1 vs 156.9 ms per step at lower clocks, profiles/r2/r2sw;
+        // QGPU_SWIZZLE_HOLD=0 lets the last phase take them)
+        static const bool hold_after = [] {
+            const char* v = std::getenv("QGPU_SWIZZLE_HOLD");
+            return !v || std::atoi(v) != 0;
+        }();
+        const bool hold = plan_mid && (phases.empty() || (hold_after && phases.size() >= 2));
         ph.mid = plan_mid && phases.size() == 1;
         if (ph.mid)
             for (int q = 0; q < kFixedLaneBits; ++q) R.push_back(q);
@@ -756,6 +765,19 @@ void QuregImpl::window_pass() {
         }
         if (!any) break;
         phases.push_back(ph);
+    }
+    // everything the pass could take waited for a middle phase (the window
+    // holds only pair ops on qubits 0-2 and what depends on them): plain
+    // phases instead
+    if (pending.empty() && plan_mid && attempt == 0) {
+        plan_mid = false;
+        phases.clear();
+        pwin.clear();
+        lane_ops = 0;
+        std::fill(taken.begin(), taken.end(), 0);
+        continue;
+    }
+    break;
     }
     if (pending.empty()) throw DeviceError("internal: reorder scheduler formed an empty pass");
     if (!phases.empty() && phases.back().mid) { // a middle phase must not be last: an empty standard one follows
