@@ -602,7 +602,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1) if achieved else None,
                          "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": round(achieved / pk["hbm_gbs"], 4) if achieved else None,
-                         "traffic": _traffic("k_tile_pass", args.local_qubits), "kernel": "k_tile_pass",
+                         "traffic": _traffic("k_tile_pass", args.local_qubits),
+                         "kernel": "k_tile_jit" if quest.lib().qgpuGetJit() else "k_tile_pass",
                          "peak_source": src, "bytes_per_launch": per_launch_bytes,
                          "avg_launch_ms": round(float(pass_ms.mean()), 4) if pass_ms.size else None,
                          "launches": int(pass_ms.size), "share_of_step": round(share, 4) if share else None,
